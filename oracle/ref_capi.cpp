@@ -1,0 +1,249 @@
+// ref_capi.cpp -- TEST INFRASTRUCTURE ONLY.
+//
+// A thin extern "C" wrapper that compiles the UNMODIFIED reference headers
+// (/root/reference/proj/include/ebic/*.hpp, included from where they lie; no
+// reference source is copied into this repository) into
+// oracle/_ref/libebic_ref.so.  tests/ use it to pin the C restatement
+// (oracle/ebic_oracle.c) and to produce golden vectors; bench.py uses it as
+// the reference CPU arm (`--impl reference`, cpu_baseline kind "reference").
+// Built by oracle/Makefile only when /root/reference is present.
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "ebic/ebic.hpp"
+
+using namespace ebic;
+
+namespace {
+
+CbfPopulation make_cbf(const std::size_t* offsets, const std::uint16_t* cols, std::size_t n) {
+    CbfPopulation pop;
+    pop.offsets.assign(offsets, offsets + n + 1);
+    pop.col_indices.assign(cols, cols + offsets[n]);
+    return pop;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ExpressionMatrix (inc/matrix.hpp:21-44) built from a row-major buffer.
+void* ref_matrix_create(const double* values, std::size_t n_rows, std::size_t n_cols) {
+    auto* m = new ExpressionMatrix(ExpressionMatrix::with_shape(n_rows, n_cols));
+    std::memcpy(m->values.data(), values, n_rows * n_cols * sizeof(double));
+    return m;
+}
+
+void ref_matrix_destroy(void* h) { delete static_cast<ExpressionMatrix*>(h); }
+
+// inc/fitness.hpp:100-118 with make_chunk_plan(n_rows, workers) (:30-39).
+int ref_count_matches(void* h, const std::size_t* offsets, const std::uint16_t* cols,
+                      std::size_t n, double eps, unsigned workers, std::uint64_t* out) {
+    const auto& m = *static_cast<ExpressionMatrix*>(h);
+    try {
+        const ChunkPlan plan = make_chunk_plan(m.n_rows, workers);
+        const auto counts = count_matches(m, make_cbf(offsets, cols, n), plan, eps);
+        std::copy(counts.begin(), counts.end(), out);
+    } catch (...) {
+        return -1;
+    }
+    return 0;
+}
+
+// inc/fitness.hpp:135-143.
+int ref_evaluate_population(void* h, const std::size_t* offsets, const std::uint16_t* cols,
+                            std::size_t n, std::uint64_t sigma, double eps, unsigned workers,
+                            double* out) {
+    const auto& m = *static_cast<ExpressionMatrix*>(h);
+    try {
+        const ChunkPlan plan = make_chunk_plan(m.n_rows, workers);
+        const auto fit =
+            evaluate_population(m, make_cbf(offsets, cols, n), plan, FitnessParams{sigma}, eps);
+        std::copy(fit.begin(), fit.end(), out);
+    } catch (...) {
+        return -1;
+    }
+    return 0;
+}
+
+double ref_fitness_score(std::uint64_t count, std::size_t len, std::uint64_t sigma) {
+    return fitness_score(count, len, FitnessParams{sigma});
+}
+
+std::uint64_t ref_default_sigma(std::size_t n_rows) { return default_sigma(n_rows); }
+
+// inc/expansion.hpp:16-23.
+std::size_t ref_assign_rows(void* h, const std::uint16_t* series, std::size_t len, double eps,
+                            std::uint64_t* rows_out) {
+    const auto& m = *static_cast<ExpressionMatrix*>(h);
+    const auto rows = assign_rows(m, std::span<const ColumnIndex>(series, len), eps);
+    std::copy(rows.begin(), rows.end(), rows_out);
+    return rows.size();
+}
+
+// inc/expansion.hpp:56-87 applied to an arbitrary (ascending) core.
+std::size_t ref_expand_bicluster(void* h, const std::uint16_t* series, std::size_t len,
+                                 const std::uint64_t* core_rows, const std::uint8_t* core_flags,
+                                 std::size_t n_core, int allow_negative, std::size_t approx_k,
+                                 double eps, std::uint64_t* rows_out, std::uint8_t* flags_out) {
+    const auto& m = *static_cast<ExpressionMatrix*>(h);
+    Bicluster core;
+    core.series.assign(series, series + len);
+    core.rows.assign(core_rows, core_rows + n_core);
+    for (std::size_t i = 0; i < n_core; ++i) core.row_flags.push_back(RowFlag(core_flags[i]));
+    ExpansionOptions opts;
+    opts.allow_negative = allow_negative != 0;
+    opts.approx_violations = approx_k;
+    const Bicluster out = expand_bicluster(m, core, opts, eps);
+    for (std::size_t i = 0; i < out.rows.size(); ++i) {
+        rows_out[i] = out.rows[i];
+        flags_out[i] = static_cast<std::uint8_t>(out.row_flags[i]);
+    }
+    return out.rows.size();
+}
+
+// inc/synthgen.hpp:114-223.  Writes the row-major values (n_rows * n_cols).
+int ref_generate(std::size_t n_rows, std::size_t n_cols, std::size_t n_blocks,
+                 const std::size_t* block_rows, const std::size_t* block_cols, int pattern,
+                 std::size_t overlap_rows, std::size_t overlap_cols, double noise_sd,
+                 std::uint64_t seed, double* values_out) {
+    ScenarioSpec spec;
+    spec.n_rows = n_rows;
+    spec.n_cols = n_cols;
+    for (std::size_t i = 0; i < n_blocks; ++i) spec.blocks.push_back({block_rows[i], block_cols[i]});
+    spec.pattern = static_cast<Pattern>(pattern);
+    spec.overlap_rows = overlap_rows;
+    spec.overlap_cols = overlap_cols;
+    spec.noise_sd = noise_sd;
+    spec.seed = seed;
+    try {
+        const GeneratedScenario g = generate(spec);
+        std::memcpy(values_out, g.matrix.values.data(), n_rows * n_cols * sizeof(double));
+    } catch (...) {
+        return -1;
+    }
+    return 0;
+}
+
+std::uint64_t ref_derive_seed(std::uint64_t master, std::uint64_t index) {
+    return Rng::derive_seed(master, index);
+}
+
+// Runs the reference GA (inc/evolution.hpp:464-520) and records every
+// evaluated batch through RunHooks::on_evaluate (:483, :503) together with
+// the reference's own count_matches result for it.  Trace file layout
+// (little endian):  repeated { u64 P; u64 offsets[P+1]; u16 cols[offsets[P]];
+// u64 counts[P] }.  Stops recording after max_batches batches (0 = all).
+// Returns the number of recorded batches, or -1 on error.
+long ref_run_trace(void* h, std::size_t population, std::size_t iterations, std::uint64_t rng_seed,
+                   double eps, std::uint64_t sigma, unsigned threads, std::size_t max_batches,
+                   const char* path) {
+    const auto& m = *static_cast<ExpressionMatrix*>(h);
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) return -1;
+    RunConfig cfg;
+    cfg.evo.population_size = population;
+    cfg.evo.max_iterations = iterations;
+    cfg.evo.rng_seed = rng_seed;
+    cfg.epsilon = eps;
+    cfg.sigma = sigma;
+    cfg.threads = threads;
+    const ChunkPlan plan = make_chunk_plan(m.n_rows, threads);
+    long recorded = 0;
+    RunHooks hooks;
+    hooks.on_evaluate = [&](std::span<const ColumnSeries> novel) {
+        if (max_batches != 0 && static_cast<std::size_t>(recorded) >= max_batches) return;
+        const CbfPopulation cbf = encode_population(novel);
+        const auto counts = count_matches(m, cbf, plan, eps);
+        const std::uint64_t p = cbf.size();
+        std::fwrite(&p, sizeof p, 1, f);
+        std::vector<std::uint64_t> off(cbf.offsets.begin(), cbf.offsets.end());
+        std::fwrite(off.data(), sizeof(std::uint64_t), off.size(), f);
+        std::fwrite(cbf.col_indices.data(), sizeof(std::uint16_t), cbf.col_indices.size(), f);
+        std::fwrite(counts.data(), sizeof(std::uint64_t), counts.size(), f);
+        ++recorded;
+    };
+    try {
+        (void)run(m, cfg, hooks);
+    } catch (...) {
+        std::fclose(f);
+        return -1;
+    }
+    std::fclose(f);
+    return recorded;
+}
+
+
+// ---- fixture generators: the input streams of the reference's own tests ----
+
+// proj/tests/acceptance_main.cpp:233-251 (property_match_counts): a 300x30
+// matrix filled from Rng(1002).normal and 500 series from Rng(1003).
+// values_out: 9000 doubles; offsets_out: 501; cols_out: capacity 3500.
+void ref_fixture_acceptance_match_counts(double* values_out, std::size_t* offsets_out,
+                                         std::uint16_t* cols_out) {
+    Rng fill(1002);
+    for (std::size_t i = 0; i < 300 * 30; ++i) values_out[i] = fill.normal(0.0, 1.0);
+    Rng rng(1003);
+    std::size_t at = 0;
+    offsets_out[0] = 0;
+    for (int i = 0; i < 500; ++i) {
+        const std::size_t len = 2 + rng.index(5);
+        ColumnSeries s;
+        while (s.size() < len) {
+            const ColumnIndex c = static_cast<ColumnIndex>(rng.index(30));
+            if (std::find(s.begin(), s.end(), c) == s.end()) s.push_back(c);
+        }
+        for (ColumnIndex c : s) cols_out[at++] = c;
+        offsets_out[i + 1] = at;
+    }
+}
+
+// proj/tests/test_fitness.cpp:111-126 (chunk invariance): trial `trial` of the
+// Rng(4242) stream.  Writes rows/cols/eps/n_series and the data; buffers sized
+// for the maxima (124 x 22 values, 10 series x 6 columns).
+void ref_fixture_fitness_trial(int trial, std::size_t* rows_out, std::size_t* cols_out,
+                               double* eps_out, std::size_t* n_series_out, double* values_out,
+                               std::size_t* offsets_out, std::uint16_t* series_cols_out) {
+    Rng rng(4242);
+    for (int t = 0; t <= trial; ++t) {
+        const std::size_t rows = 5 + rng.index(120);
+        const std::size_t cols = 3 + rng.index(20);
+        ExpressionMatrix m = ExpressionMatrix::with_shape(rows, cols);
+        for (double& v : m.values) v = rng.normal();
+        const double epsilon = rng.chance(0.3) ? rng.real(0.0, 0.5) : 0.0;
+        std::vector<ColumnSeries> series(1 + rng.index(10));
+        for (ColumnSeries& s : series) {
+            const std::size_t len = 2 + rng.index(std::min<std::size_t>(cols, 6) - 1);
+            while (s.size() < len) {
+                const auto col = static_cast<ColumnIndex>(rng.index(cols));
+                if (std::find(s.begin(), s.end(), col) == s.end()) s.push_back(col);
+            }
+        }
+        if (t != trial) continue;
+        *rows_out = rows;
+        *cols_out = cols;
+        *eps_out = epsilon;
+        *n_series_out = series.size();
+        std::memcpy(values_out, m.values.data(), rows * cols * sizeof(double));
+        std::size_t at = 0;
+        offsets_out[0] = 0;
+        for (std::size_t i = 0; i < series.size(); ++i) {
+            for (ColumnIndex c : series[i]) series_cols_out[at++] = c;
+            offsets_out[i + 1] = at;
+        }
+    }
+}
+
+// Matrix of Rng(seed).normal() draws, row-major (test_expansion.cpp:21-26).
+void ref_fixture_random_matrix(std::size_t rows, std::size_t cols, std::uint64_t seed,
+                               double* values_out) {
+    Rng rng(seed);
+    for (std::size_t i = 0; i < rows * cols; ++i) values_out[i] = rng.normal(0.0, 1.0);
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+// run_driver.cpp -- TEST INFRASTRUCTURE ONLY (drop-in proof).
+//
+// One end-to-end EBIC run written purely against the reference's public API:
+// generate a scenario (inc/synthgen.hpp:114), run the GA (inc/evolution.hpp:464),
+// finalize Steps 6-7 (inc/io.hpp:164) and write the results JSON
+// (inc/io.hpp:64-78), mirroring `ebic run` (proj/tools/ebic_main.cpp:151-197).
+//
+// oracle/Makefile compiles this file twice from the same source:
+//   oracle/_ref/ebic_ref_run     -I /root/reference/proj/include only
+//                                (pure reference CPU path)
+//   oracle/_ref/ebic_dropin_run  -I include  -I /root/reference/proj/include
+//                                i.e. the repo's include/ebic/fitness.hpp and
+//                                include/ebic/expansion.hpp shadow the
+//                                reference's, so the reference's own run() and
+//                                finalize_biclusters() call the B200 library.
+// tests/test_gpu_dropin.py requires the two JSON files to be byte-identical.
+//
+// Usage: run_driver key=value ... out=<path>
+//   rows cols blocks=RxC[,RxC...] pattern overlap seed population iterations
+//   rng_seed epsilon overlap_threshold threads sigma
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <sstream>
+#include <string>
+
+#include "ebic/ebic.hpp"
+
+#ifndef EBIC_DRIVER_NAME
+#define EBIC_DRIVER_NAME "reference"
+#endif
+
+using namespace ebic;
+
+int main(int argc, char** argv) {
+    std::map<std::string, std::string> kv = {
+        {"rows", "500"},        {"cols", "100"},          {"blocks", "50x10,50x10,50x10"},
+        {"pattern", "trend_preserving"}, {"overlap", "0"}, {"seed", "1"},
+        {"noise", "0"},         {"population", "600"},    {"iterations", "1000"},
+        {"rng_seed", "1"},      {"epsilon", "0"},         {"overlap_threshold", "0.75"},
+        {"threads", "1"},       {"sigma", "0"},           {"allow_negative", "1"},
+        {"approx", "1"},        {"threshold", "auto"},    {"out", "out.json"}};
+    for (int i = 1; i < argc; ++i) {
+        std::string a = argv[i];
+        auto eq = a.find('=');
+        if (eq == std::string::npos) {
+            std::fprintf(stderr, "bad argument %s\n", argv[i]);
+            return 2;
+        }
+        kv[a.substr(0, eq)] = a.substr(eq + 1);
+    }
+    try {
+        ScenarioSpec spec;
+        spec.n_rows = std::stoull(kv["rows"]);
+        spec.n_cols = std::stoull(kv["cols"]);
+        std::stringstream bs(kv["blocks"]);
+        std::string item;
+        while (std::getline(bs, item, ',')) {
+            auto x = item.find('x');
+            spec.blocks.push_back({std::stoull(item.substr(0, x)), std::stoull(item.substr(x + 1))});
+        }
+        spec.pattern = pattern_from_name(kv["pattern"]);
+        spec.overlap_rows = spec.overlap_cols = std::stoull(kv["overlap"]);
+        spec.noise_sd = std::stod(kv["noise"]);
+        spec.seed = std::stoull(kv["seed"]);
+        const GeneratedScenario data = generate(spec);
+
+        RunConfig cfg;
+        cfg.evo.population_size = std::stoull(kv["population"]);
+        cfg.evo.max_iterations = std::stoull(kv["iterations"]);
+        cfg.evo.rng_seed = std::stoull(kv["rng_seed"]);
+        cfg.evo.overlap_threshold = std::stod(kv["overlap_threshold"]);
+        cfg.epsilon = std::stod(kv["epsilon"]);
+        cfg.threads = static_cast<unsigned>(std::stoul(kv["threads"]));
+        cfg.sigma = std::stoull(kv["sigma"]);
+        const RunResult result = run(data.matrix, cfg);
+
+        ExpansionOptions exp;
+        exp.allow_negative = kv["allow_negative"] != "0";
+        exp.approx_violations = std::stoull(kv["approx"]);
+        OutputOptions out_opts;
+        if (kv["threshold"] == "none") out_opts.threshold = OutputOptions::Threshold::kNone;
+        const std::vector<Bicluster> biclusters = finalize_biclusters(
+            result.top_rank, data.matrix, exp, cfg.epsilon, out_opts, result.sigma_used);
+
+        RunSummary summary;
+        summary.generations = result.generations;
+        summary.series_evaluated = result.series_evaluated;
+        summary.sigma = result.sigma_used;
+        summary.tabu_terminated = result.tabu_terminated;
+        write_biclusters_file(kv["out"], biclusters, &summary);
+        std::fprintf(stderr, "[%s] generations=%zu series_evaluated=%llu biclusters=%zu\n",
+                     EBIC_DRIVER_NAME, result.generations,
+                     static_cast<unsigned long long>(result.series_evaluated), biclusters.size());
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "error: %s\n", e.what());
+        return 1;
+    }
+    return 0;
+}

@@ -1,0 +1,60 @@
+"""In-tree build of the product library ``libebic_b200.so`` (sm_100a only).
+
+Invoked by ``__graft_entry__.build()`` and ``python -m paper_1801_03039_b200._build``.
+nvcc cross-compiles for sm_100a without a GPU.  The library statically links the
+CUDA runtime so the .so that travels with gpurun is self-contained.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+REPO = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libebic_b200.so"
+SOURCES = [CSRC / "ebic_b200.cu", CSRC / "synth.cpp"]
+DEPS = SOURCES + [CSRC / "kernels.cuh", REPO / "include" / "ebic_b200.h"]
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# -ffp-contract=off: host-side fitness/synth arithmetic must not fuse into FMAs
+# (bit-exact parity with the reference's x86-64 SSE2 arithmetic).
+FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",
+         "-Xcompiler", "-fPIC,-O2,-ffp-contract=off,-fvisibility=hidden",
+         "-Xptxas", "-warn-spills"]
+
+
+def needs_build() -> bool:
+    if not LIB.exists():
+        return True
+    t = LIB.stat().st_mtime
+    return any(p.stat().st_mtime > t for p in DEPS)
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    if not force and not needs_build():
+        return LIB
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-o", str(tmp), *map(str, SOURCES)]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, cwd=str(PKG))
+    os.replace(tmp, LIB)
+    return LIB
+
+
+def ptxas_report() -> str:
+    """Register / spill / shared-memory report of every kernel (-Xptxas -v)."""
+    cmd = [NVCC, *ARCH, *FLAGS, "-Xptxas", "-v", "-c", "-o", "/dev/null", str(SOURCES[0])]
+    r = subprocess.run(cmd, capture_output=True, text=True, cwd=str(PKG))
+    return r.stderr
+
+
+if __name__ == "__main__":
+    if "--ptxas" in sys.argv:
+        print(ptxas_report())
+    else:
+        print(build(verbose=True, force="--force" in sys.argv))

@@ -1,0 +1,863 @@
+// ebic_b200.cu -- context management and the C ABI (include/ebic_b200.h).
+//
+// Replaces, B200-first, the reference's evaluation engine and its CPU runtime:
+//   make_chunk_plan / ThreadPool / count_chunk / count_matches / evaluate_population
+//     (/root/reference/proj/include/ebic/fitness.hpp:30-143, parallel.hpp:17-89)
+//   assign_rows / trend_violations / expand_bicluster
+//     (/root/reference/proj/include/ebic/expansion.hpp:16-87)
+// Row chunks become per-device row shards held column-major in HBM; one kernel
+// launch evaluates a whole generation against a shard.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/ebic_b200.h"
+#include "kernels.cuh"
+
+using namespace ebic_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error {
+    int status;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int status, const std::string& msg) { throw Error{status, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        fail(EBIC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+#define CK(x) cuda_check((x), #x)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return EBIC_OK;
+    } catch (const Error& e) {
+        g_last_error = e.msg;
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return EBIC_ERR_RUNTIME;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return EBIC_ERR_RUNTIME;
+    }
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p)
+            fail(EBIC_ERR_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+class DeviceGuard {
+  public:
+    explicit DeviceGuard(int dev) {
+        CK(cudaGetDevice(&prev_));
+        if (prev_ != dev) CK(cudaSetDevice(dev));
+        dev_ = dev;
+    }
+    ~DeviceGuard() {
+        if (prev_ != dev_) cudaSetDevice(prev_);
+    }
+
+  private:
+    int prev_ = 0, dev_ = 0;
+};
+
+constexpr int kNCW = 16;       // consumer warps per count CTA
+constexpr size_t kMaxSeriesPerLaunch = 4096;
+constexpr size_t kMaxLenPerLaunch = 16384;
+constexpr int kThreads = (kNCW + 1) * 32;
+
+// Kernel configuration of the TMA count kernel for one shard.
+struct CountConfig {
+    int rpg = 0;        // rows per tile (0 = direct kernel)
+    int rpl = 1;        // rows per lane
+    int stages = 0;
+    uint32_t box_cols = 0, n_boxes = 0, stage_bytes = 0;
+};
+
+struct Tables {
+    uint64_t sigma = 0;
+    size_t n = 0;
+    double* d_log = nullptr;
+    double* d_exp = nullptr;
+};
+
+struct Shard {
+    int device = 0;
+    size_t row_begin = 0;  // global first row
+    size_t rows = 0;
+    size_t ld = 0;         // padded leading dimension (multiple of 64)
+    double* d_mat = nullptr;
+    cudaStream_t stream = nullptr;
+    int sm_count = 0;
+    int max_smem = 0;
+    // TMA descriptors, one per row-tile height (index log2(rpg)).
+    CUtensorMap tmap[6];
+    bool tmap_ok[6] = {false, false, false, false, false, false};
+    // scratch
+    unsigned char* d_in = nullptr;
+    size_t d_in_cap = 0;
+    unsigned long long* d_acc = nullptr;
+    size_t acc_cap = 0;
+    unsigned int* d_done = nullptr;
+    unsigned char* d_out = nullptr;
+    size_t d_out_cap = 0;
+    unsigned char* h_pin = nullptr;
+    size_t h_pin_cap = 0;
+    Tables tables;
+    int last_grid = 0;
+    CountConfig last_cfg;
+};
+
+void grow_device(unsigned char** p, size_t* cap, size_t need) {
+    if (need <= *cap) return;
+    if (*p) CK(cudaFree(*p));
+    *p = nullptr;
+    size_t n = std::max(need, *cap * 2);
+    n = (n + 255) & ~size_t(255);
+    CK(cudaMalloc(p, n));
+    *cap = n;
+}
+
+void grow_pinned(unsigned char** p, size_t* cap, size_t need) {
+    if (need <= *cap) return;
+    if (*p) CK(cudaFreeHost(*p));
+    *p = nullptr;
+    size_t n = std::max(need, *cap * 2);
+    n = (n + 255) & ~size_t(255);
+    CK(cudaMallocHost(p, n));
+    *cap = n;
+}
+
+void ensure_acc(Shard& s, size_t P) {
+    if (P <= s.acc_cap) return;
+    if (s.d_acc) CK(cudaFree(s.d_acc));
+    s.d_acc = nullptr;
+    const size_t n = std::max(P, s.acc_cap * 2);
+    CK(cudaMalloc(&s.d_acc, n * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(s.d_acc, 0, n * sizeof(unsigned long long), s.stream));
+    s.acc_cap = n;
+}
+
+}  // namespace
+
+struct ebic_ctx {
+    size_t n_rows = 0;      // rows held
+    size_t n_cols = 0;
+    size_t row_begin = 0;   // global row of shards[0]
+    size_t total_rows = 0;  // rows of the full matrix (fitness tables, sigma)
+    std::vector<Shard> shards;
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// matrix upload: row-major host/device buffer -> column-major padded shard
+// ---------------------------------------------------------------------------
+void upload_shard(Shard& s, const double* src_rows, size_t n_cols, bool src_on_device) {
+    DeviceGuard g(s.device);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, s.device));
+    s.sm_count = prop.multiProcessorCount;
+    CK(cudaDeviceGetAttribute(&s.max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, s.device));
+    CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    s.ld = std::max<size_t>(64, (s.rows + 63) / 64 * 64);
+    CK(cudaMalloc(&s.d_mat, s.ld * n_cols * sizeof(double)));
+    CK(cudaMalloc(&s.d_done, sizeof(unsigned int)));
+    CK(cudaMemsetAsync(s.d_done, 0, sizeof(unsigned int), s.stream));
+
+    // Stage <= 64 MB of rows at a time (and < 2^21 rows: grid.y limit).
+    size_t chunk = std::max<size_t>(32, (64ull << 20) / (n_cols * sizeof(double)));
+    chunk = std::min<size_t>(chunk, 1u << 20);
+    chunk = (chunk + 31) / 32 * 32;
+    double* staging = nullptr;
+    if (!src_on_device) CK(cudaMalloc(&staging, std::min(chunk, s.rows) * n_cols * sizeof(double) + 8));
+    for (size_t r0 = 0; r0 < s.ld; r0 += chunk) {
+        const size_t out_rows = std::min(chunk, s.ld - r0);
+        const size_t in_rows = r0 < s.rows ? std::min(out_rows, s.rows - r0) : 0;
+        const double* in = nullptr;
+        if (in_rows) {
+            if (src_on_device) {
+                in = src_rows + r0 * n_cols;
+            } else {
+                CK(cudaMemcpyAsync(staging, src_rows + r0 * n_cols, in_rows * n_cols * sizeof(double),
+                                   cudaMemcpyHostToDevice, s.stream));
+                in = staging;
+            }
+        }
+        dim3 grid((unsigned)((n_cols + 31) / 32), (unsigned)((out_rows + 31) / 32));
+        transpose_pad_kernel<<<grid, dim3(32, 8), 0, s.stream>>>(in, in_rows, n_cols, s.d_mat + r0,
+                                                                 s.ld, out_rows);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(s.stream));
+    if (staging) CK(cudaFree(staging));
+}
+
+int log2i(int x) {
+    int l = 0;
+    while ((1 << l) < x) ++l;
+    return l;
+}
+
+const CUtensorMap& tensor_map(Shard& s, size_t n_cols, const CountConfig& cfg) {
+    const int idx = log2i(cfg.rpg);
+    if (!s.tmap_ok[idx]) {
+        cuuint64_t dims[2] = {(cuuint64_t)s.ld, (cuuint64_t)n_cols};
+        cuuint64_t strides[1] = {(cuuint64_t)(s.ld * sizeof(double))};
+        cuuint32_t box[2] = {(cuuint32_t)cfg.rpg, cfg.box_cols};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = tensor_map_encoder()(&s.tmap[idx], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, s.d_mat,
+                                          dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(EBIC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        s.tmap_ok[idx] = true;
+    }
+    return s.tmap[idx];
+}
+
+// Shared-memory bytes of a TMA count launch.
+size_t tma_smem_bytes(const CountConfig& c, size_t P, size_t L) {
+    return 128 + size_t(c.stages) * c.stage_bytes + 2 * kMaxStages * sizeof(uint64_t) +
+           count_meta_bytes((uint32_t)P, (uint32_t)L);
+}
+
+// Picks the row-tile height: the tallest tile (coalesced 128-byte column slices
+// at 16 rows) that still leaves a >= 3-deep TMA ring in shared memory.
+CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L) {
+    CountConfig best;
+    if (env_int("EBIC_FORCE_DIRECT", 0)) return best;
+    const int want_rpg = env_int("EBIC_RPG", 0);
+    const int want_rpl = env_int("EBIC_RPL", 0);
+    const int want_stages = env_int("EBIC_STAGES", 0);
+    const size_t budget = (size_t)s.max_smem;
+    for (int min_stages : {3, 2}) {
+        for (int rpg : {16, 32, 8, 4}) {
+            if (want_rpg && rpg != want_rpg) continue;
+            CountConfig c;
+            c.rpg = rpg;
+            c.rpl = want_rpl ? want_rpl : 1;
+            if (c.rpl > 1 && rpg < 4) c.rpl = 1;
+            const uint32_t nb = (uint32_t)((n_cols + 255) / 256);
+            uint32_t bc = (uint32_t)((n_cols + nb - 1) / nb);
+            bc = (bc + 7) / 8 * 8;  // 128-byte aligned box destinations for every rpg
+            c.n_boxes = nb;
+            c.box_cols = bc;
+            const size_t sb = size_t(rpg) * 8 * bc * nb;
+            if (sb >= (1u << 20)) continue;
+            c.stage_bytes = (uint32_t)sb;
+            int st = want_stages ? want_stages : kMaxStages;
+            for (; st >= min_stages; --st) {
+                c.stages = st;
+                if (tma_smem_bytes(c, P, L) <= budget) break;
+            }
+            if (st < min_stages) continue;
+            // Deep rings beyond 4 stages buy nothing once HBM is saturated.
+            if (!want_stages) c.stages = std::min(c.stages, 4);
+            return c;
+        }
+    }
+    return best;  // rpg == 0 -> direct kernel
+}
+
+template <int RPG, int RPL, bool E0>
+void launch_tma_t(const CUtensorMap& tm, const CountParams& p, int grid, size_t smem,
+                  cudaStream_t st) {
+    auto k = count_tma_kernel<RPG, RPL, kNCW, E0>;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<grid, kThreads, smem, st>>>(tm, p);
+}
+
+template <int RPG, int RPL>
+void launch_tma_e(bool e0, const CUtensorMap& tm, const CountParams& p, int grid, size_t smem,
+                  cudaStream_t st) {
+    if (e0) launch_tma_t<RPG, RPL, true>(tm, p, grid, smem, st);
+    else launch_tma_t<RPG, RPL, false>(tm, p, grid, smem, st);
+}
+
+void launch_tma(const CountConfig& c, bool e0, const CUtensorMap& tm, const CountParams& p,
+                int grid, size_t smem, cudaStream_t st) {
+    switch (c.rpg * 10 + c.rpl) {
+        case 321: launch_tma_e<32, 1>(e0, tm, p, grid, smem, st); break;
+        case 322: launch_tma_e<32, 2>(e0, tm, p, grid, smem, st); break;
+        case 161: launch_tma_e<16, 1>(e0, tm, p, grid, smem, st); break;
+        case 162: launch_tma_e<16, 2>(e0, tm, p, grid, smem, st); break;
+        case 81: launch_tma_e<8, 1>(e0, tm, p, grid, smem, st); break;
+        case 82: launch_tma_e<8, 2>(e0, tm, p, grid, smem, st); break;
+        case 41: launch_tma_e<4, 1>(e0, tm, p, grid, smem, st); break;
+        case 42: launch_tma_e<4, 2>(e0, tm, p, grid, smem, st); break;
+        default: fail(EBIC_ERR_RUNTIME, "unsupported count-kernel configuration");
+    }
+    CK(cudaGetLastError());
+}
+
+// Host-built Eq. 1 tables (same glibc log/exp2 as fitness.hpp:129,131).
+const Tables& ensure_tables(Shard& s, uint64_t sigma, size_t total_rows) {
+    Tables& t = s.tables;
+    if (t.d_log && t.sigma == sigma && t.n == total_rows + 1) return t;
+    DeviceGuard g(s.device);
+    const size_t n = total_rows + 1;
+    std::vector<double> lg(n, 0.0), ex(n, 1.0);
+    for (size_t c = 2; c < n; ++c) lg[c] = std::log(static_cast<double>(c - 1));
+    for (size_t c = 0; c < n; ++c)
+        if (c < sigma) ex[c] = std::exp2(static_cast<double>(c) - static_cast<double>(sigma));
+    if (t.n != n) {
+        if (t.d_log) CK(cudaFree(t.d_log));
+        if (t.d_exp) CK(cudaFree(t.d_exp));
+        t.d_log = t.d_exp = nullptr;
+        CK(cudaMalloc(&t.d_log, n * sizeof(double)));
+        CK(cudaMalloc(&t.d_exp, n * sizeof(double)));
+    }
+    CK(cudaMemcpyAsync(t.d_log, lg.data(), n * sizeof(double), cudaMemcpyHostToDevice, s.stream));
+    CK(cudaMemcpyAsync(t.d_exp, ex.data(), n * sizeof(double), cudaMemcpyHostToDevice, s.stream));
+    CK(cudaStreamSynchronize(s.stream));
+    t.sigma = sigma;
+    t.n = n;
+    return t;
+}
+
+// Launches the count kernel for one shard.  All pointers are device pointers.
+void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t* d_cols, size_t P,
+                  size_t L, double eps, uint64_t* d_counts, double* d_fit, uint64_t sigma,
+                  cudaStream_t st) {
+    if (P == 0) return;
+    if (P > 0xffffffffull || L > 0xffffffffull || s.rows > 0xffffffffull)
+        fail(EBIC_ERR_INVALID_ARGUMENT, "population or shard too large for one launch");
+    ensure_acc(s, P);
+    CountParams p{};
+    p.offsets = d_off;
+    p.cols = d_cols;
+    p.n_series = (uint32_t)P;
+    p.total_len = (uint32_t)L;
+    p.n_rows = (uint32_t)s.rows;
+    p.n_cols = (uint32_t)ctx.n_cols;
+    p.eps = eps;
+    p.sigma = sigma;
+    p.acc = s.d_acc;
+    p.done = s.d_done;
+    p.counts_out = d_counts;
+    p.fitness_out = d_fit;
+    p.matrix = s.d_mat;
+    p.ld = (uint32_t)s.ld;
+    if (d_fit) {
+        const Tables& t = ensure_tables(s, sigma, ctx.total_rows);
+        p.logt = t.d_log;
+        p.expt = t.d_exp;
+    }
+    const bool e0 = (eps == 0.0);
+    CountConfig c = choose_config(s, ctx.n_cols, P, L);
+    if (c.rpg) {
+        p.box_cols = c.box_cols;
+        p.n_boxes = c.n_boxes;
+        p.stage_bytes = c.stage_bytes;
+        p.stages = (uint32_t)c.stages;
+        p.n_tiles = (uint32_t)((s.rows + c.rpg - 1) / c.rpg);
+        const size_t smem = tma_smem_bytes(c, P, L);
+        int grid = std::min<int>((int)p.n_tiles, s.sm_count);
+        const int g_env = env_int("EBIC_GRID", 0);
+        if (g_env > 0) grid = std::min<int>(g_env, (int)p.n_tiles);
+        s.last_grid = grid;
+        s.last_cfg = c;
+        launch_tma(c, e0, tensor_map(s, ctx.n_cols, c), p, grid, smem, st);
+    } else {
+        const size_t smem = 8 * P + 16;
+        if (smem > (size_t)s.max_smem) fail(EBIC_ERR_INVALID_ARGUMENT, "population too large for one launch");
+        const int grid = (int)((s.rows + 255) / 256);
+        s.last_grid = grid;
+        s.last_cfg = c;
+        if (e0) {
+            CK(cudaFuncSetAttribute(count_direct_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            count_direct_kernel<true><<<grid, 256, smem, st>>>(p);
+        } else {
+            CK(cudaFuncSetAttribute(count_direct_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            count_direct_kernel<false><<<grid, 256, smem, st>>>(p);
+        }
+        CK(cudaGetLastError());
+    }
+}
+
+// Reference-side validation of a host CBF before it reaches the device:
+// offsets start at 0 and never decrease (cbf.hpp:70-79) and every column index
+// addresses the matrix (cbf.hpp:32-37).  count_matches itself does not check
+// (its caller guarantees validity); the device must not read out of bounds, so
+// the C ABI rejects what would be undefined behaviour in the reference.
+void validate_cbf(const size_t* off, const uint16_t* cols, size_t P, size_t n_cols) {
+    if (!off) fail(EBIC_ERR_INVALID_ARGUMENT, "corrupt CBF");
+    if (off[0] != 0) fail(EBIC_ERR_RUNTIME, "corrupt CBF");
+    for (size_t p = 0; p < P; ++p)
+        if (off[p + 1] < off[p]) fail(EBIC_ERR_RUNTIME, "corrupt CBF");
+    const size_t L = off[P];
+    if (L && !cols) fail(EBIC_ERR_INVALID_ARGUMENT, "corrupt CBF");
+    for (size_t i = 0; i < L; ++i)
+        if (cols[i] >= n_cols) fail(EBIC_ERR_INVALID_ARGUMENT, "invalid series");
+}
+
+// Packs the CBF into pinned memory, copies it to every shard, launches the
+// count kernel per shard and brings counts (and fitness) back.
+void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_t P, double eps,
+                   bool want_fit, uint64_t sigma, uint64_t* counts_out, double* fit_out) {
+    if (P == 0) return;
+    validate_cbf(off, cols, P, ctx.n_cols);
+    const size_t L = off[P];
+    const size_t off_bytes = (P + 1) * sizeof(uint64_t);
+    const size_t cols_at = (off_bytes + 15) & ~size_t(15);
+    const size_t in_bytes = cols_at + L * sizeof(uint16_t);
+    const size_t out_bytes = P * sizeof(uint64_t) * 2;
+    const bool single = ctx.shards.size() == 1;
+    for (Shard& s : ctx.shards) {
+        DeviceGuard g(s.device);
+        grow_pinned(&s.h_pin, &s.h_pin_cap, in_bytes + out_bytes + 16);
+        grow_device(&s.d_in, &s.d_in_cap, in_bytes);
+        grow_device(&s.d_out, &s.d_out_cap, out_bytes);
+        static_assert(sizeof(size_t) == sizeof(uint64_t), "size_t must be 64-bit");
+        std::memcpy(s.h_pin, off, off_bytes);
+        if (L) std::memcpy(s.h_pin + cols_at, cols, L * sizeof(uint16_t));
+        CK(cudaMemcpyAsync(s.d_in, s.h_pin, in_bytes, cudaMemcpyHostToDevice, s.stream));
+        uint64_t* d_counts = reinterpret_cast<uint64_t*>(s.d_out);
+        double* d_fit = (single && want_fit) ? reinterpret_cast<double*>(s.d_out + P * 8) : nullptr;
+        const auto* d_off = reinterpret_cast<const uint64_t*>(s.d_in);
+        const auto* d_cols = reinterpret_cast<const uint16_t*>(s.d_in + cols_at);
+        // One launch per slice of at most kMaxSeriesPerLaunch series /
+        // kMaxLenPerLaunch columns (the per-CTA work list lives in shared
+        // memory); a generation (P ~ 600) is always a single launch.
+        for (size_t s0 = 0; s0 < P;) {
+            size_t s1 = s0;
+            while (s1 < P && s1 - s0 < kMaxSeriesPerLaunch && off[s1 + 1] - off[s0] <= kMaxLenPerLaunch) ++s1;
+            if (s1 == s0) s1 = s0 + 1;  // a single over-long series still gets its own launch
+            launch_count(ctx, s, d_off + s0, d_cols, s1 - s0, off[s1] - off[s0], eps, d_counts + s0,
+                         d_fit ? d_fit + s0 : nullptr, sigma, s.stream);
+            s0 = s1;
+        }
+        CK(cudaMemcpyAsync(s.h_pin + in_bytes, s.d_out, d_fit ? out_bytes : P * 8,
+                           cudaMemcpyDeviceToHost, s.stream));
+    }
+    std::vector<uint64_t> total;
+    if (!single) total.assign(P, 0);
+    for (Shard& s : ctx.shards) {
+        DeviceGuard g(s.device);
+        CK(cudaStreamSynchronize(s.stream));
+        const uint64_t* c = reinterpret_cast<const uint64_t*>(s.h_pin + in_bytes);
+        if (single) {
+            if (counts_out) std::memcpy(counts_out, c, P * 8);
+            if (want_fit) std::memcpy(fit_out, s.h_pin + in_bytes + P * 8, P * 8);
+        } else {
+            for (size_t p = 0; p < P; ++p) total[p] += c[p];  // exact integer reduction
+        }
+    }
+    if (!single) {
+        if (counts_out) std::memcpy(counts_out, total.data(), P * 8);
+        if (want_fit)
+            for (size_t p = 0; p < P; ++p)
+                fit_out[p] = ebic_fitness_score(total[p], off[p + 1] - off[p], sigma);
+    }
+}
+
+// Membership bitmasks of every shard gathered into global word order.
+void host_membership(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_t S, double eps,
+                     size_t k, uint64_t* ex, uint64_t* ng, uint64_t* ap) {
+    if (S == 0) return;
+    validate_cbf(off, cols, S, ctx.n_cols);
+    if (S > 65535) fail(EBIC_ERR_INVALID_ARGUMENT, "too many series for one membership launch");
+    const size_t L = off[S];
+    const size_t words_total = (ctx.n_rows + 63) / 64;
+    const size_t off_bytes = (S + 1) * 8, cols_at = (off_bytes + 15) & ~size_t(15);
+    const size_t in_bytes = cols_at + L * 2;
+    uint64_t* outs[3] = {ex, ng, ap};
+    for (Shard& s : ctx.shards) {
+        DeviceGuard g(s.device);
+        const size_t words = (s.rows + 63) / 64;
+        const size_t bits_bytes = S * words * 8;
+        grow_pinned(&s.h_pin, &s.h_pin_cap, in_bytes);
+        grow_device(&s.d_in, &s.d_in_cap, in_bytes);
+        grow_device(&s.d_out, &s.d_out_cap, 3 * bits_bytes);
+        std::memcpy(s.h_pin, off, off_bytes);
+        if (L) std::memcpy(s.h_pin + cols_at, cols, L * 2);
+        CK(cudaMemcpyAsync(s.d_in, s.h_pin, in_bytes, cudaMemcpyHostToDevice, s.stream));
+        uint64_t* d_bits[3];
+        for (int i = 0; i < 3; ++i)
+            d_bits[i] = outs[i] ? reinterpret_cast<uint64_t*>(s.d_out + i * bits_bytes) : nullptr;
+        dim3 grid((unsigned)((s.rows + 255) / 256), (unsigned)S);
+        const auto* d_off = reinterpret_cast<const uint64_t*>(s.d_in);
+        const auto* d_cols = reinterpret_cast<const uint16_t*>(s.d_in + cols_at);
+        if (eps == 0.0)
+            membership_kernel<true><<<grid, 256, 0, s.stream>>>(s.d_mat, (uint32_t)s.ld, (uint32_t)s.rows, d_off, d_cols, eps, (uint64_t)k, (uint32_t)words, d_bits[0], d_bits[1], d_bits[2]);
+        else
+            membership_kernel<false><<<grid, 256, 0, s.stream>>>(s.d_mat, (uint32_t)s.ld, (uint32_t)s.rows, d_off, d_cols, eps, (uint64_t)k, (uint32_t)words, d_bits[0], d_bits[1], d_bits[2]);
+        CK(cudaGetLastError());
+        const size_t word0 = (s.row_begin - ctx.row_begin) / 64;
+        for (int i = 0; i < 3; ++i) {
+            if (!outs[i]) continue;
+            CK(cudaMemcpy2DAsync(outs[i] + word0, words_total * 8, d_bits[i], words * 8, words * 8, S,
+                                 cudaMemcpyDeviceToHost, s.stream));
+        }
+    }
+    for (Shard& s : ctx.shards) {
+        DeviceGuard g(s.device);
+        CK(cudaStreamSynchronize(s.stream));
+    }
+}
+
+Shard& single_shard(ebic_ctx* ctx) {
+    if (!ctx) fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+    if (ctx->shards.size() != 1) fail(EBIC_ERR_INVALID_ARGUMENT, "device-pointer API needs a single-shard context");
+    return ctx->shards[0];
+}
+
+void free_shard(Shard& s) {
+    cudaSetDevice(s.device);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    cudaFree(s.d_mat);
+    cudaFree(s.d_in);
+    cudaFree(s.d_acc);
+    cudaFree(s.d_done);
+    cudaFree(s.d_out);
+    if (s.h_pin) cudaFreeHost(s.h_pin);
+    cudaFree(s.tables.d_log);
+    cudaFree(s.tables.d_exp);
+    if (s.stream) cudaStreamDestroy(s.stream);
+}
+
+ebic_ctx* make_ctx(const double* rows_ptr, size_t n_rows, size_t n_cols, size_t total_rows,
+                   size_t row_begin, const int* devices, int n_devices, bool on_device) {
+    if (n_rows == 0 || total_rows == 0) fail(EBIC_ERR_INVALID_ARGUMENT, "matrix has no rows");
+    if (n_cols == 0) fail(EBIC_ERR_INVALID_ARGUMENT, "matrix has no columns");
+    if (n_cols > 65535) fail(EBIC_ERR_INVALID_ARGUMENT, "too many columns (at most 65535 supported)");
+    if (!rows_ptr) fail(EBIC_ERR_INVALID_ARGUMENT, "null matrix");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        (void)cudaGetLastError();
+        fail(EBIC_ERR_NO_DEVICE, "no CUDA device available");
+    }
+    std::vector<int> devs;
+    if (!devices || n_devices <= 0) devs.push_back(0);
+    else devs.assign(devices, devices + n_devices);
+    for (int d : devs)
+        if (d < 0 || d >= ndev) fail(EBIC_ERR_INVALID_ARGUMENT, "invalid device id");
+    auto ctx = std::make_unique<ebic_ctx>();
+    ctx->n_rows = n_rows;
+    ctx->n_cols = n_cols;
+    ctx->row_begin = row_begin;
+    ctx->total_rows = total_rows;
+    // 64-row aligned contiguous shards (bitmask words concatenate across shards).
+    size_t per = (n_rows + devs.size() - 1) / devs.size();
+    per = (per + 63) / 64 * 64;
+    size_t r = 0;
+    for (size_t i = 0; i < devs.size() && r < n_rows; ++i) {
+        Shard s;
+        s.device = devs[i];
+        s.row_begin = row_begin + r;
+        s.rows = std::min(per, n_rows - r);
+        ctx->shards.push_back(s);
+        r += s.rows;
+    }
+    try {
+        for (Shard& s : ctx->shards)
+            upload_shard(s, rows_ptr + (s.row_begin - row_begin) * n_cols, n_cols, on_device);
+    } catch (...) {
+        for (Shard& s : ctx->shards) free_shard(s);
+        throw;
+    }
+    return ctx.release();
+}
+
+// Row list of the set bits of `bits` (ctx-local rows) as global row ids.
+template <class F>
+void for_each_bit(const uint64_t* bits, size_t words, F&& f) {
+    for (size_t w = 0; w < words; ++w) {
+        uint64_t x = bits[w];
+        while (x) {
+            const int b = __builtin_ctzll(x);
+            f(w * 64 + b);
+            x &= x - 1;
+        }
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* ebic_last_error(void) { return g_last_error.c_str(); }
+
+int ebic_abi_version(void) { return EBIC_B200_ABI_VERSION; }
+
+int ebic_device_count(int* count_out) {
+    return guarded([&] {
+        if (!count_out) fail(EBIC_ERR_INVALID_ARGUMENT, "null output");
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) {
+            (void)cudaGetLastError();
+            n = 0;
+        }
+        *count_out = n;
+    });
+}
+
+int ebic_ctx_create(const double* row_major, size_t n_rows, size_t n_cols, const int* devices,
+                    int n_devices, ebic_ctx** ctx_out) {
+    return guarded([&] {
+        if (!ctx_out) fail(EBIC_ERR_INVALID_ARGUMENT, "null output");
+        *ctx_out = make_ctx(row_major, n_rows, n_cols, n_rows, 0, devices, n_devices, false);
+    });
+}
+
+int ebic_ctx_create_shard(const double* row_major_shard, size_t shard_rows, size_t n_cols,
+                          size_t total_rows, size_t row_begin, int device, ebic_ctx** ctx_out) {
+    return guarded([&] {
+        if (!ctx_out) fail(EBIC_ERR_INVALID_ARGUMENT, "null output");
+        if (row_begin + shard_rows > total_rows) fail(EBIC_ERR_INVALID_ARGUMENT, "shard outside matrix");
+        *ctx_out = make_ctx(row_major_shard, shard_rows, n_cols, total_rows, row_begin, &device, 1, false);
+    });
+}
+
+int ebic_ctx_create_shard_device(const double* d_row_major, size_t shard_rows, size_t n_cols,
+                                 size_t total_rows, size_t row_begin, int device,
+                                 ebic_ctx** ctx_out) {
+    return guarded([&] {
+        if (!ctx_out) fail(EBIC_ERR_INVALID_ARGUMENT, "null output");
+        if (row_begin + shard_rows > total_rows) fail(EBIC_ERR_INVALID_ARGUMENT, "shard outside matrix");
+        *ctx_out = make_ctx(d_row_major, shard_rows, n_cols, total_rows, row_begin, &device, 1, true);
+    });
+}
+
+int ebic_ctx_destroy(ebic_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        for (Shard& s : ctx->shards) free_shard(s);
+        delete ctx;
+    });
+}
+
+int ebic_ctx_get_info(const ebic_ctx* ctx, ebic_ctx_info* info) {
+    return guarded([&] {
+        if (!ctx || !info) fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+        std::memset(info, 0, sizeof(*info));
+        info->n_rows = ctx->n_rows;
+        info->n_cols = ctx->n_cols;
+        info->row_begin = ctx->row_begin;
+        info->total_rows = ctx->total_rows;
+        info->n_shards = (int)ctx->shards.size();
+        const Shard& s = ctx->shards[0];
+        info->rows_per_tile = s.last_cfg.rpg;
+        info->stages = s.last_cfg.stages;
+        info->grid = s.last_grid;
+        info->device_bytes = s.ld * ctx->n_cols * sizeof(double);
+        info->sm_count = s.sm_count;
+    });
+}
+
+int ebic_count_matches(ebic_ctx* ctx, const size_t* offsets, const uint16_t* cols,
+                       size_t n_series, double eps, uint64_t* counts_out) {
+    return guarded([&] {
+        if (!ctx) fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+        if (n_series && !counts_out) fail(EBIC_ERR_INVALID_ARGUMENT, "null output");
+        host_evaluate(*ctx, offsets, cols, n_series, eps, false, 0, counts_out, nullptr);
+    });
+}
+
+int ebic_evaluate_population(ebic_ctx* ctx, const size_t* offsets, const uint16_t* cols,
+                             size_t n_series, uint64_t sigma, double eps, uint64_t* counts_out,
+                             double* fitness_out) {
+    return guarded([&] {
+        if (!ctx) fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+        if (n_series && !fitness_out) fail(EBIC_ERR_INVALID_ARGUMENT, "null output");
+        host_evaluate(*ctx, offsets, cols, n_series, eps, true, sigma, counts_out, fitness_out);
+    });
+}
+
+double ebic_fitness_score(uint64_t match_count, size_t series_len, uint64_t sigma) {
+    // fitness.hpp:124-133, verbatim arithmetic.
+    if (match_count <= 1) return 0.0;
+    double f = static_cast<double>(series_len) * std::log(static_cast<double>(match_count - 1));
+    if (match_count < sigma)
+        f *= std::exp2(static_cast<double>(match_count) - static_cast<double>(sigma));
+    return f > 0.0 ? f : 0.0;
+}
+
+uint64_t ebic_default_sigma(size_t n_rows) {
+    const uint64_t scaled = static_cast<uint64_t>((n_rows + 49) / 50);  // fitness.hpp:48-52
+    return scaled < 4 ? 4 : scaled;
+}
+
+int ebic_count_matches_device(ebic_ctx* ctx, const uint64_t* d_offsets, const uint16_t* d_cols,
+                              size_t n_series, size_t total_len, double eps, uint64_t sigma,
+                              uint64_t* d_counts_out, double* d_fitness_out, void* stream) {
+    return guarded([&] {
+        Shard& s = single_shard(ctx);
+        DeviceGuard g(s.device);
+        if (n_series && (!d_offsets || !d_counts_out)) fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+        // Fused Eq. 1 only when the counts are final (whole-matrix context).
+        const bool whole = ctx->row_begin == 0 && ctx->n_rows == ctx->total_rows;
+        if (d_fitness_out && !whole) fail(EBIC_ERR_INVALID_ARGUMENT, "fitness needs reduced counts on a shard context");
+        if (n_series > kMaxSeriesPerLaunch || total_len > kMaxLenPerLaunch)
+            fail(EBIC_ERR_INVALID_ARGUMENT, "device batch exceeds 4096 series / 16384 columns; split it");
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s.stream;
+        launch_count(*ctx, s, d_offsets, d_cols, n_series, total_len, eps, d_counts_out, d_fitness_out,
+                     sigma, st);
+    });
+}
+
+int ebic_fitness_device(ebic_ctx* ctx, const uint64_t* d_counts, const uint64_t* d_offsets,
+                        size_t n_series, uint64_t sigma, double* d_fitness_out, void* stream) {
+    return guarded([&] {
+        Shard& s = single_shard(ctx);
+        DeviceGuard g(s.device);
+        if (n_series == 0) return;
+        const Tables& t = ensure_tables(s, sigma, ctx->total_rows);
+        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s.stream;
+        fitness_kernel<<<(unsigned)((n_series + 255) / 256), 256, 0, st>>>(
+            d_counts, d_offsets, (uint32_t)n_series, sigma, t.d_log, t.d_exp, d_fitness_out);
+        CK(cudaGetLastError());
+    });
+}
+
+int ebic_membership_bits(ebic_ctx* ctx, const size_t* offsets, const uint16_t* cols,
+                         size_t n_series, double eps, size_t approx_k, uint64_t* exact_bits,
+                         uint64_t* neg_bits, uint64_t* approx_bits) {
+    return guarded([&] {
+        if (!ctx) fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+        host_membership(*ctx, offsets, cols, n_series, eps, approx_k, exact_bits, neg_bits, approx_bits);
+    });
+}
+
+int ebic_assign_rows(ebic_ctx* ctx, const uint16_t* series, size_t len, double eps,
+                     uint64_t* rows_out, size_t* n_out) {
+    return guarded([&] {
+        if (!ctx || !n_out) fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+        if (len == 0) fail(EBIC_ERR_INVALID_ARGUMENT, "invalid series");
+        const size_t off[2] = {0, len};
+        const size_t words = (ctx->n_rows + 63) / 64;
+        std::vector<uint64_t> ex(words);
+        host_membership(*ctx, off, series, 1, eps, 0, ex.data(), nullptr, nullptr);
+        size_t n = 0;
+        for_each_bit(ex.data(), words, [&](size_t r) { rows_out[n++] = ctx->row_begin + r; });
+        *n_out = n;
+    });
+}
+
+int ebic_expand_bicluster(ebic_ctx* ctx, const uint16_t* series, size_t len,
+                          const uint64_t* core_rows, const uint8_t* core_flags, size_t n_core,
+                          int allow_negative, size_t approx_k, double eps, uint64_t* rows_out,
+                          uint8_t* flags_out, size_t* n_out) {
+    return guarded([&] {
+        if (!ctx || !n_out) fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+        if (len == 0) fail(EBIC_ERR_INVALID_ARGUMENT, "invalid series");
+        const size_t off[2] = {0, len};
+        const size_t words = (ctx->n_rows + 63) / 64;
+        std::vector<uint64_t> ng(words, 0), ap(words, 0);
+        const bool want_neg = allow_negative != 0, want_ap = approx_k > 0;
+        if (want_neg || want_ap)
+            host_membership(*ctx, off, series, 1, eps, approx_k, nullptr, want_neg ? ng.data() : nullptr,
+                            want_ap ? ap.data() : nullptr);
+        // Candidate rows (ctx-local): negative first, then approximate; drop core rows.
+        std::vector<uint64_t> cand(words);
+        for (size_t w = 0; w < words; ++w) cand[w] = ng[w] | ap[w];
+        for (size_t i = 0; i < n_core; ++i) {
+            const uint64_t r = core_rows[i];
+            if (r >= ctx->row_begin && r < ctx->row_begin + ctx->n_rows) {
+                const uint64_t l = r - ctx->row_begin;
+                cand[l / 64] &= ~(uint64_t(1) << (l % 64));
+            }
+        }
+        // Merge ascending core rows with the added rows (expansion.hpp:73-86).
+        size_t n = 0, ci = 0;
+        auto emit_core_upto = [&](uint64_t row) {
+            while (ci < n_core && core_rows[ci] < row) {
+                rows_out[n] = core_rows[ci];
+                flags_out[n] = core_flags[ci];
+                ++n, ++ci;
+            }
+        };
+        for_each_bit(cand.data(), words, [&](size_t l) {
+            const uint64_t row = ctx->row_begin + l;
+            emit_core_upto(row);
+            const bool neg = (ng[l / 64] >> (l % 64)) & 1;
+            rows_out[n] = row;
+            flags_out[n] = neg ? EBIC_ROW_NEGATIVE : EBIC_ROW_APPROXIMATE;
+            ++n;
+        });
+        emit_core_upto(~uint64_t(0));
+        while (ci < n_core) {
+            rows_out[n] = core_rows[ci];
+            flags_out[n] = core_flags[ci];
+            ++n, ++ci;
+        }
+        *n_out = n;
+    });
+}
+
+int ebic_resolve_expand_batch(ebic_ctx* ctx, const size_t* offsets, const uint16_t* cols,
+                              size_t n_series, int allow_negative, size_t approx_k, double eps,
+                              uint64_t* rows_out, uint8_t* flags_out, size_t* row_counts) {
+    return guarded([&] {
+        if (!ctx) fail(EBIC_ERR_INVALID_ARGUMENT, "null context");
+        if (n_series == 0) return;
+        const size_t words = (ctx->n_rows + 63) / 64;
+        std::vector<uint64_t> ex(n_series * words), ng(n_series * words, 0), ap(n_series * words, 0);
+        const bool want_neg = allow_negative != 0, want_ap = approx_k > 0;
+        host_membership(*ctx, offsets, cols, n_series, eps, approx_k, ex.data(),
+                        want_neg ? ng.data() : nullptr, want_ap ? ap.data() : nullptr);
+        size_t n = 0;
+        for (size_t s = 0; s < n_series; ++s) {
+            const size_t start = n;
+            const uint64_t* e = ex.data() + s * words;
+            const uint64_t* g = ng.data() + s * words;
+            const uint64_t* a = ap.data() + s * words;
+            for (size_t w = 0; w < words; ++w) {
+                uint64_t x = e[w] | g[w] | a[w];
+                while (x) {
+                    const int b = __builtin_ctzll(x);
+                    const uint64_t bit = uint64_t(1) << b;
+                    rows_out[n] = ctx->row_begin + w * 64 + b;
+                    flags_out[n] = (e[w] & bit) ? EBIC_ROW_EXACT
+                                   : (g[w] & bit) ? EBIC_ROW_NEGATIVE
+                                                  : EBIC_ROW_APPROXIMATE;
+                    ++n;
+                    x &= x - 1;
+                }
+            }
+            row_counts[s] = n - start;
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,281 @@
+"""GPU parity: the sm_100a path through the C ABI against the reference.
+
+Every comparison is exact: counts ==, fitness bitwise == (fp64 bit patterns),
+membership rows/flags ==.  Expected values come from the reference itself
+(golden fixtures generated from the unmodified reference headers) or from the
+CPU oracle (oracle/ebic_oracle.c, pinned to the reference by
+tests/test_oracle_golden.py) on the same seeded inputs.
+"""
+import os
+from contextlib import contextmanager
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1801_03039_b200 as eb
+from golden_io import TRACE_NAMES, acceptance, expansion_cases, fitness_trials, trace
+
+pytestmark = pytest.mark.gpu
+port = oracle.Port()
+
+# Every count-kernel configuration the library can select (rows-per-tile x
+# rows-per-lane, plus the unstaged direct kernel).
+KERNEL_CONFIGS = [dict(EBIC_RPG=str(g), EBIC_RPL=str(l)) for g in (32, 16, 8, 4) for l in (1, 2)] + [
+    dict(EBIC_FORCE_DIRECT="1")]
+
+
+@contextmanager
+def env(**kw):
+    old = {k: os.environ.get(k) for k in kw}
+    os.environ.update(kw)
+    try:
+        yield
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def cbf(series):
+    off = np.zeros(len(series) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(s) for s in series])
+    return eb.CbfPopulation(off, np.array([c for s in series for c in s], dtype=np.uint16))
+
+
+def bits_equal(a, b):
+    return (np.asarray(a, np.float64).view(np.uint64) == np.asarray(b, np.float64).view(np.uint64)).all()
+
+
+def random_population(rng, n_cols, P, max_len=9):
+    return [list(map(int, rng.choice(n_cols, size=int(rng.integers(2, min(n_cols, max_len) + 1)),
+                                     replace=False))) for _ in range(P)]
+
+
+# ---------------------------------------------------------------------------
+def test_smoke_small():
+    rng = np.random.default_rng(0)
+    v = rng.standard_normal((300, 30))
+    pop = cbf(random_population(rng, 30, 200))
+    with eb.Evaluator(v) as ev:
+        fit, counts = ev.evaluate_population(pop, eb.FitnessParams(6), 0.0, return_counts=True)
+        info = ev.info()
+    c, f = port.evaluate_population(v, pop.offsets, pop.col_indices, 6, 0.0)
+    assert (counts == c).all() and bits_equal(fit, f)
+    assert info.rows_per_tile > 0 and info.grid > 0
+
+
+def test_acceptance_golden_all_eps():  # acceptance_main.cpp:233-292
+    z = acceptance()
+    pop = eb.CbfPopulation(z["offsets"], z["cols"])
+    with eb.Evaluator(z["values"]) as ev:
+        for i, eps in enumerate(z["eps"]):
+            assert (ev.count_matches(pop, eps) == z[f"counts_{i}"]).all()
+            fit = ev.evaluate_population(pop, eb.FitnessParams(int(z["sigma"])), eps)
+            assert bits_equal(fit, z[f"fitness_{i}"])
+
+
+def test_fitness_trials_golden():  # test_fitness.cpp:111-137
+    for v, off, cols, eps, counts in fitness_trials():
+        with eb.Evaluator(v) as ev:
+            assert (ev.count_matches(eb.CbfPopulation(off, cols), eps) == counts).all()
+
+
+@pytest.mark.parametrize("name", TRACE_NAMES)
+def test_trace_golden(name):
+    """Every batch of a recorded reference GA run: counts and fitness bit-exact."""
+    t = trace(name)
+    with eb.Evaluator(t.matrix()) as ev:
+        for off, cols, counts, fit in t.batches:
+            f, c = ev.evaluate_population(eb.CbfPopulation(off, cols), eb.FitnessParams(t.sigma),
+                                          t.eps, return_counts=True)
+            assert (c == counts).all()
+            assert bits_equal(f, fit)
+
+
+@pytest.mark.parametrize("cfg", KERNEL_CONFIGS, ids=lambda d: "-".join(f"{k}={v}" for k, v in d.items()))
+@pytest.mark.parametrize("name", ["c1e", "c3", "c4"])
+def test_every_kernel_config_on_traces(cfg, name):
+    t = trace(name)
+    v = t.matrix()
+    with env(**cfg):
+        with eb.Evaluator(v) as ev:
+            for off, cols, counts, fit in t.batches[:3]:
+                f, c = ev.evaluate_population(eb.CbfPopulation(off, cols), eb.FitnessParams(t.sigma),
+                                              t.eps, return_counts=True)
+                assert (c == counts).all()
+                assert bits_equal(f, fit)
+
+
+@pytest.mark.parametrize("cfg", KERNEL_CONFIGS[:8:3] + KERNEL_CONFIGS[-1:], ids=str)
+def test_edge_cases_vs_oracle(cfg):
+    """Ragged row counts, ties, +-0, NaN/inf cells, odd eps values, len-1 series."""
+    rng = np.random.default_rng(7)
+    with env(**cfg):
+        for rows in (1, 2, 15, 16, 17, 31, 33, 63, 64, 65, 127, 129, 1000, 4097):
+            n_cols = int(rng.integers(3, 90))
+            v = np.round(rng.standard_normal((rows, n_cols)), 1)
+            flat = v.ravel()
+            k = max(1, flat.size // 50)
+            flat[rng.choice(flat.size, k, replace=False)] = rng.choice(
+                [np.nan, np.inf, -np.inf, 0.0, -0.0], k)
+            series = random_population(rng, n_cols, int(rng.integers(1, 300)))
+            series[0] = [series[0][0]]  # length-1 series: no adjacent pair -> every row matches
+            pop = cbf(series)
+            with eb.Evaluator(v) as ev:
+                for eps in (0.0, -0.0, 1e-9, 0.1, -0.05, np.inf, np.nan, 1e300):
+                    got = ev.count_matches(pop, eps)
+                    want = port.count_matches(v, pop.offsets, pop.col_indices, eps)
+                    assert (got == want).all(), (rows, n_cols, eps)
+
+
+def test_empty_population_and_errors():
+    v = np.random.default_rng(1).standard_normal((100, 10))
+    with eb.Evaluator(v) as ev:
+        assert ev.count_matches(eb.CbfPopulation()).size == 0
+        with pytest.raises(ValueError, match="invalid series"):
+            ev.count_matches(cbf([[0, 10]]))
+        with pytest.raises(RuntimeError, match="corrupt CBF"):
+            ev.count_matches(eb.CbfPopulation(np.array([0, 3, 2], np.uint64),
+                                              np.array([0, 1, 2], np.uint16)))
+    with pytest.raises(ValueError, match="matrix has no rows"):
+        eb.Evaluator(np.zeros((0, 5)))
+
+
+def test_large_population_is_split_exactly():
+    """P above one launch's shared-memory work list (4096 series)."""
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal((3000, 120))
+    pop = cbf(random_population(rng, 120, 9000))
+    with eb.Evaluator(v) as ev:
+        f, c = ev.evaluate_population(pop, eb.FitnessParams(60), 1e-9, return_counts=True)
+    wc, wf = port.evaluate_population(v, pop.offsets, pop.col_indices, 60, 1e-9)
+    assert (c == wc).all() and bits_equal(f, wf)
+
+
+def test_wide_matrix_direct_path():
+    """Many columns: config selection falls back to the unstaged kernel."""
+    rng = np.random.default_rng(4)
+    v = rng.standard_normal((700, 9000))
+    pop = cbf(random_population(rng, 9000, 400, max_len=12))
+    with eb.Evaluator(v) as ev:
+        got = ev.count_matches(pop, 0.05)
+    assert (got == port.count_matches(v, pop.offsets, pop.col_indices, 0.05)).all()
+
+
+def test_row_shards_on_one_device_are_partition_invariant():
+    """devices=[0,0,0]: three 64-row-aligned shards on one GPU, exact host reduction."""
+    t = trace("c3")
+    v = t.matrix()
+    with eb.Evaluator(v, devices=[0, 0, 0]) as ev:
+        assert ev.info().n_shards == 3
+        for off, cols, counts, fit in t.batches[:4]:
+            f, c = ev.evaluate_population(eb.CbfPopulation(off, cols), eb.FitnessParams(t.sigma),
+                                          t.eps, return_counts=True)
+            assert (c == counts).all() and bits_equal(f, fit)
+
+
+def test_shard_contexts_sum_to_whole():
+    """One-process-per-GPU layout: per-shard partial counts + reduction == reference."""
+    t = trace("c2_scale")
+    v = t.matrix()
+    bounds = [0, 320, 640, 1000]
+    off, cols, counts, fit = t.batches[2]
+    pop = eb.CbfPopulation(off, cols)
+    total = np.zeros_like(counts)
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        with eb.Evaluator(v[lo:hi], shard=(lo, v.shape[0])) as ev:
+            total += ev.count_matches(pop, t.eps)
+    assert (total == counts).all()
+
+
+def test_device_pointer_api_with_fused_fitness():
+    import torch
+    from paper_1801_03039_b200 import _lib
+    t = trace("c1e")
+    v = t.matrix()
+    with eb.Evaluator(v) as ev:
+        for off, cols, counts, fit in t.batches[:3]:
+            d_off = torch.from_numpy(off.astype(np.int64)).cuda()
+            d_cols = torch.from_numpy(cols.astype(np.int16)).cuda()
+            d_cnt = torch.zeros(len(counts), dtype=torch.int64, device="cuda")
+            d_fit = torch.zeros(len(counts), dtype=torch.float64, device="cuda")
+            st = torch.cuda.current_stream().cuda_stream
+            _lib.check(_lib.lib.ebic_count_matches_device(
+                ev.handle, d_off.data_ptr(), d_cols.data_ptr(), len(counts), int(off[-1]), t.eps,
+                t.sigma, d_cnt.data_ptr(), d_fit.data_ptr(), st))
+            torch.cuda.synchronize()
+            assert (d_cnt.cpu().numpy().astype(np.uint64) == counts).all()
+            assert bits_equal(d_fit.cpu().numpy(), fit)
+            d_fit2 = torch.zeros_like(d_fit)
+            _lib.check(_lib.lib.ebic_fitness_device(ev.handle, d_cnt.data_ptr(), d_off.data_ptr(),
+                                                    len(counts), t.sigma, d_fit2.data_ptr(), st))
+            torch.cuda.synchronize()
+            assert bits_equal(d_fit2.cpu().numpy(), fit)
+
+
+# ---- membership (Steps 6-7) ------------------------------------------------
+def test_expansion_golden():
+    for case in expansion_cases():
+        with eb.Evaluator(case["matrix"]) as ev:
+            core = ev.resolve_bicluster(case["series"], 1.0, case["eps"])
+            assert core.rows == [int(r) for r in case["core"]]
+            grown = ev.expand_bicluster(core, eb.ExpansionOptions(case["allow_negative"],
+                                                                  case["approx_k"]), case["eps"])
+            assert grown.rows == [int(r) for r in case["rows"]]
+            assert [int(f) for f in grown.row_flags] == [int(f) for f in case["flags"]]
+            (rows, flags), = ev.resolve_expand_batch(
+                [list(map(int, case["series"]))],
+                eb.ExpansionOptions(case["allow_negative"], case["approx_k"]), case["eps"])
+            assert list(rows) == [int(r) for r in case["rows"]]
+            assert list(flags) == [int(f) for f in case["flags"]]
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0, 0]])
+def test_membership_bits_vs_oracle(devices):
+    rng = np.random.default_rng(8)
+    for rows in (1, 63, 64, 65, 200, 1000, 5001):
+        n_cols = int(rng.integers(3, 40))
+        v = np.round(rng.standard_normal((rows, n_cols)), 1)
+        series = random_population(rng, n_cols, 20)
+        with eb.Evaluator(v, devices=devices) as ev:
+            for eps, k in ((0.0, 1), (0.1, 2), (1e-9, 0)):
+                ex, ng, ap = ev.membership_bits(cbf(series), eps, k)
+                for i, s in enumerate(series):
+                    e2, n2, a2 = port.membership_bits(v, s, eps, k)
+                    assert (ex[i] == e2).all() and (ng[i] == n2).all() and (ap[i] == a2).all()
+
+
+def test_expand_with_arbitrary_core_vs_oracle():
+    rng = np.random.default_rng(9)
+    v = np.round(rng.standard_normal((700, 12)), 1)
+    with eb.Evaluator(v) as ev:
+        for trial in range(30):
+            s = random_population(rng, 12, 1)[0]
+            core = sorted(map(int, rng.choice(700, size=int(rng.integers(0, 40)), replace=False)))
+            flags = [int(x) for x in rng.integers(0, 3, size=len(core))]
+            b = eb.Bicluster(core, s, 2.0, [eb.RowFlag(f) for f in flags])
+            for opts in (eb.ExpansionOptions(), eb.ExpansionOptions(False, 2), eb.ExpansionOptions(True, 0)):
+                g = ev.expand_bicluster(b, opts, 0.05)
+                wr, wf = port.expand_bicluster(v, s, core, flags, opts.allow_negative,
+                                               opts.approx_violations, 0.05)
+                assert g.rows == wr and [int(f) for f in g.row_flags] == wf
+
+
+def test_finalize_biclusters_c4_top_series():
+    """io.hpp:164-178 over the C4 matrix: one batched launch for 100 series."""
+    t = trace("c4")
+    v = t.matrix()
+    off, cols, counts, fit = t.batches[-1]
+    order = np.argsort(-fit, kind="stable")[:100]
+    series = [list(map(int, cols[int(off[i]):int(off[i + 1])])) for i in order]
+    entries = [(s, float(fit[i])) for s, i in zip(series, order)]
+    m = eb.ExpressionMatrix(v)
+    out = eb.finalize_biclusters(entries, m, eb.ExpansionOptions(), t.eps, 0.0)
+    assert len(out) == 100
+    for b in out[:12]:
+        core = port.assign_rows(v, b.series, t.eps)
+        wr, wf = port.expand_bicluster(v, b.series, core, [0] * len(core), True, 1, t.eps)
+        assert b.rows == wr and [int(f) for f in b.row_flags] == wf
