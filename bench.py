@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark of the EBIC fitness-evaluation hot path on B200.
+
+Metric (BASELINE.json): biclusters evaluated/sec (+ fitness-kernel GB/s vs
+roofline).  A step is one generation's novel batch (P = 575 series, the
+reference's `series_evaluated` unit, evolution.hpp:486,506) evaluated against
+every row of the matrix: per-series match counts + Eq. 1 fitness
+(fitness.hpp:100-143).
+
+Workload (default, N=1): BASELINE config 4 -- the 20,000 x 500 synthetic
+matrix (ebic::generate, 5 planted 600x20 trend blocks, seed 2026; regenerated
+bit-identically by the product generator) and the novel batches of a real
+reference GA run on it (tests/golden/trace_c4.npz, recorded through
+RunHooks::on_evaluate), eps = 1e-9, sigma = default 400.
+
+Arms
+  (default)          the B200 path.  `value`: inputs resident in HBM, one count
+                     kernel (fused fitness) per step, CUDA events on the launch
+                     stream, L2 flushed between steps (outside the events).
+                     `e2e`: the public API with host buffers
+                     (Evaluator.evaluate_population -> ebic_evaluate_population:
+                     pinned H2D of the CBF, kernel, D2H of counts + fitness).
+  --impl reference   the reference's own CPU implementation (oracle/_ref, the
+                     unmodified headers compiled here) on all host threads.
+
+Multi-GPU (torchrun, one process per GPU): rows are sharded (64-row aligned);
+each rank counts its shard, counts are all-reduced (NCCL, int64 sum), then the
+Eq. 1 kernel runs on the reduced counts.  Time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+METRIC = "biclusters evaluated/sec"
+UNIT = "biclusters/s"
+
+WORKLOADS = {
+    # name: trace fixture (holds the scenario spec, eps and the reference batches)
+    "c4": "c4",
+    "c5": "c5",
+    "c3": "c3",
+    "c1": "c1e",
+}
+
+
+def load_workload(name: str):
+    from golden_io import trace
+    t = trace(WORKLOADS[name])
+    return t
+
+
+def hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int = 0):
+        self.dev = device_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(",") for r in out.strip().splitlines() if r.strip()]
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for i, n in enumerate(names):
+                if len(r) > 4 + i and "Active" in r[4 + i] and "Not" not in r[4 + i]:
+                    reasons.add(n)
+        busy = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(rows: int, off: np.ndarray, cols: np.ndarray) -> int:
+    """rows x U x 8 (fp64 cells of the distinct columns the
+    launch references) + CBF in + counts/fitness out."""
+    P = len(off) - 1
+    U = len(np.unique(cols))
+    return rows * U * 8 + (P + 1) * 8 + len(cols) * 2 + P * 8 * 2
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference(t, values, batches, steps, warmup, budget_s=60.0, threads=None):
+    """The reference CPU implementation on this host (oracle/_ref when built,
+    else the C restatement).  Each step evaluates a bounded sample of a batch
+    (a prefix of its series) so the whole run stays within ~budget_s."""
+    import oracle
+    threads = threads or os.cpu_count() or 1
+    if oracle.REF_LIB.exists():
+        ref = oracle.Ref()
+        m = ref.matrix(values)
+        kind = "reference"
+
+        def run(off, cols):
+            return ref.evaluate_population(m, off, cols, t.sigma, t.eps, workers=threads)
+    else:
+        port = oracle.Port()
+        kind, threads = "port", 1
+
+        def run(off, cols):
+            return port.evaluate_population(values, off, cols, t.sigma, t.eps)[1]
+
+    # Warm-up: >= 2 s of multi-threaded work (cold vCPUs).
+    t0 = time.perf_counter()
+    full = []
+    while time.perf_counter() - t0 < 2.0 or len(full) < max(1, warmup):
+        off, cols, _, _ = batches[len(full) % len(batches)]
+        a = time.perf_counter()
+        run(off, cols)
+        full.append((time.perf_counter() - a) / (len(off) - 1))
+    per_series = min(full)
+    P = len(batches[0][0]) - 1
+    sample = int(max(1, min(P, budget_s / max(steps, 1) / per_series)))
+    done = 0
+    t0 = time.perf_counter()
+    for k in range(steps):
+        off, cols, _, _ = batches[k % len(batches)]
+        n = min(sample, len(off) - 1)
+        sub_off = off[:n + 1]
+        run(sub_off, cols[:int(sub_off[-1])])
+        done += n
+    el = time.perf_counter() - t0
+    return {"value": done / el, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{steps} steps x first {sample} of {P} series of a C4 GA batch "
+                      f"(all {values.shape[0]} rows, eps={t.eps}); {threads} threads"}
+
+
+# ---------------------------------------------------------------------------
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    t = load_workload(args.workload)
+    values = t.matrix()
+    cb = cpu_reference(t, values, t.batches, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(t, args),
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(t, args):
+    s = t.spec
+    return {"workload": f"{args.workload}: synthetic {s['rows']}x{s['cols']} "
+                        f"({len(s['blocks'])} planted {s['blocks'][0][0]}x{s['blocks'][0][1]} trend blocks, "
+                        f"seed {s['seed']}), reference GA novel batches (population 600)",
+            "rows": s["rows"], "cols": s["cols"], "series_per_step": len(t.batches[0][0]) - 1,
+            "eps": t.eps, "sigma": t.sigma, "l2": "flushed between timed steps (512 MB write)",
+            "parallelism": f"rows sharded over {args.gpus} GPU(s)"}
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_1801_03039_b200 as eb
+    from paper_1801_03039_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+
+    t = load_workload(args.workload)
+    values = t.matrix()
+    R = values.shape[0]
+    lo, hi = eb.shard_range(R, world, rank)
+    sharded = world > 1
+    if sharded:
+        ev = eb.Evaluator(values[lo:hi], devices=[local], shard=(lo, R))
+    else:
+        ev = eb.Evaluator(values, devices=[local])
+
+    stream = torch.cuda.current_stream(dev)
+    st = stream.cuda_stream
+    # Device-resident inputs: every batch's CBF in HBM.
+    dev_batches = []
+    for off, cols, counts, fit in t.batches:
+        dev_batches.append(dict(
+            P=len(off) - 1, L=int(off[-1]),
+            off=torch.from_numpy(off.astype(np.int64)).to(dev),
+            cols=torch.from_numpy(cols.view(np.int16)).to(dev),
+            counts=torch.zeros(len(off) - 1, dtype=torch.int64, device=dev),
+            fit=torch.zeros(len(off) - 1, dtype=torch.float64, device=dev),
+            bytes=algorithmic_bytes(hi - lo, off, cols), want=(counts, fit)))
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step(b):
+        if sharded:
+            _lib.check(_lib.lib.ebic_count_matches_device(
+                ev.handle, b["off"].data_ptr(), b["cols"].data_ptr(), b["P"], b["L"], t.eps,
+                t.sigma, b["counts"].data_ptr(), None, st))
+            dist.all_reduce(b["counts"], op=dist.ReduceOp.SUM)
+            _lib.check(_lib.lib.ebic_fitness_device(
+                ev.handle, b["counts"].data_ptr(), b["off"].data_ptr(), b["P"], t.sigma,
+                b["fit"].data_ptr(), st))
+        else:
+            _lib.check(_lib.lib.ebic_count_matches_device(
+                ev.handle, b["off"].data_ptr(), b["cols"].data_ptr(), b["P"], b["L"], t.eps,
+                t.sigma, b["counts"].data_ptr(), b["fit"].data_ptr(), st))
+
+    launches_per_step = 2 if sharded else 1
+
+    # warm-up + correctness gate on every batch (bit-exact vs the reference trace)
+    for k in range(max(args.warmup, len(dev_batches))):
+        step(dev_batches[k % len(dev_batches)])
+    torch.cuda.synchronize()
+    for b in dev_batches:
+        step(b)
+        torch.cuda.synchronize()
+        c = b["counts"].cpu().numpy().astype(np.uint64)
+        f = b["fit"].cpu().numpy()
+        assert (c == b["want"][0]).all(), "count mismatch vs reference"
+        assert (f.view(np.uint64) == b["want"][1].view(np.uint64)).all(), "fitness mismatch"
+
+    # ---- timed: device-resident inputs ----
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if sharded:
+        dist.barrier()
+    torch.cuda.synchronize()
+    series = 0
+    nbytes = 0
+    for k in range(args.steps):
+        b = dev_batches[k % len(dev_batches)]
+        flush.zero_()                       # evict L2 (outside the events)
+        torch.cuda._sleep(100_000)          # keep the queue ahead of the host launch path
+        starts[k].record(stream)
+        step(b)
+        ends[k].record(stream)
+        series += b["P"]
+        nbytes += b["bytes"]
+    torch.cuda.synchronize()
+    if sharded:
+        dist.barrier()
+    times = [s.elapsed_time(e) for s, e in zip(starts, ends)]  # ms
+    total_ms = float(sum(times))
+    clk = clocks.stop() if rank == 0 else None
+    if sharded:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    value = series / (total_ms / 1e3)
+
+    # kernel-only timing for the roofline (single launch per step when unsharded)
+    avg_launch_ms = total_ms / args.steps if not sharded else None
+    peak, peak_src = hbm_peak()
+    info = ev.info()
+
+    # ---- e2e: public API, host buffers, H2D + kernel + D2H each step ----
+    pops = [eb.CbfPopulation(off, cols) for off, cols, _, _ in t.batches]
+    e2e_val = None
+    h2d = d2h = 0
+    if not sharded:
+        params = eb.FitnessParams(t.sigma)
+        for k in range(max(3, args.warmup)):
+            ev.evaluate_population(pops[k % len(pops)], params, t.eps)
+        el = 0.0
+        n_e2e = 0
+        for k in range(args.steps):
+            pop = pops[k % len(pops)]
+            flush.zero_()
+            torch.cuda.synchronize()
+            a = time.perf_counter()
+            ev.evaluate_population(pop, params, t.eps)  # returns host fitness (synchronous)
+            el += time.perf_counter() - a
+            n_e2e += pop.size()
+            h2d += (pop.size() + 1) * 8 + len(pop.col_indices) * 2
+            d2h += pop.size() * 16
+        e2e_val = n_e2e / el
+        h2d //= args.steps
+        d2h //= args.steps
+
+    cb = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cb = cpu_reference(t, values, t.batches, steps=min(args.steps, 40), warmup=2,
+                           budget_s=args.cpu_budget)
+
+    if rank == 0:
+        avg_bytes = nbytes / args.steps
+        roof = None
+        if avg_launch_ms:
+            achieved = avg_bytes / (avg_launch_ms / 1e3) / 1e9
+            traffic = None
+            tp = ROOT / "profiles" / f"traffic_{args.workload}.json"
+            if tp.exists():
+                traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "algorithmic_bytes_per_launch": avg_bytes, "peak_source": peak_src,
+                    "kernel": "count_tma_kernel (fused Eq. 1 epilogue)",
+                    "avg_launch_us": avg_launch_ms * 1e3}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generator, bit-identical) + reference GA batches",
+            "config": workload_config(t, args),
+            "roofline": roof, "cpu_baseline": cb, "clocks": clk,
+            "e2e": ({"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                     "d2h_bytes_per_step": d2h} if e2e_val else None),
+            "gpu_launches": args.steps * launches_per_step,
+            "kernel_config": {"rows_per_tile": info.rows_per_tile, "stages": info.stages,
+                              "grid": info.grid, "sm_count": info.sm_count},
+            "parity": "counts and fitness bit-exact vs reference trace on every batch",
+        }
+        print(json.dumps(line), flush=True)
+    ev.close()
+    if sharded:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0,
+                    help="seconds of timed CPU reference work for cpu_baseline")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -30,7 +30,7 @@ __all__ = [
     "decode_population", "make_chunk_plan", "default_sigma", "fitness_score", "row_matches",
     "count_matches", "evaluate_population", "assign_rows", "trend_violations",
     "resolve_bicluster", "expand_bicluster", "finalize_biclusters", "Evaluator", "synth_generate",
-    "device_count",
+    "device_count", "shard_range",
 ]
 
 ColumnSeries = List[int]
@@ -209,6 +209,21 @@ def _as_cbf_arrays(pop: CbfPopulation):
     if cols.size == 0:
         cols = np.zeros(1, dtype=np.uint16)
     return off, cols
+
+
+def shard_range(total_rows: int, world_size: int, rank: int) -> tuple:
+    """Contiguous row shard [lo, hi) of one rank: make_chunk_plan's contiguous
+    chunking (fitness.hpp:30-39) with 64-row aligned boundaries, so per-shard
+    membership bitmask words concatenate.  Counts are partition invariant
+    (fitness.hpp:17-19), so any world size gives identical results."""
+    if total_rows == 0:
+        raise ValueError("matrix has no rows")
+    if world_size <= 0 or not (0 <= rank < world_size):
+        raise ValueError("invalid rank")
+    per = -(-total_rows // world_size)
+    per = -(-per // 64) * 64
+    lo = min(rank * per, total_rows)
+    return lo, min(lo + per, total_rows)
 
 
 class Evaluator:

@@ -300,7 +300,15 @@ template <int RPG, int RPL, bool E0>
 void launch_tma_t(const CUtensorMap& tm, const CountParams& p, int grid, size_t smem,
                   cudaStream_t st) {
     auto k = count_tma_kernel<RPG, RPL, kNCW, E0>;
-    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // The attribute is per function and device; set it only when it grows so
+    // the per-generation launch path makes no extra driver calls.
+    static int smem_set[64] = {0};
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64 || (int)smem > smem_set[dev]) {
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (dev >= 0 && dev < 64) smem_set[dev] = (int)smem;
+    }
     k<<<grid, kThreads, smem, st>>>(tm, p);
 }
 

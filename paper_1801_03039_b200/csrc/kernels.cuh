@@ -381,8 +381,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 
 // ---------------------------------------------------------------------------
 // K1 (direct): no staging; for matrices too wide for a shared-memory tile.
-// Block = 8 warps over 256 consecutive rows; warps stride over series; loads
-// are coalesced column slices of the column-major matrix (L1/L2 reuse).
+// Block = 8 warps over 256 consecutive rows (32 per warp); every warp walks
+// every series for its rows; loads are coalesced 256-byte column slices of the
+// column-major matrix (L1/L2 reuse across series).
 // ---------------------------------------------------------------------------
 template <bool kEpsZero>
 __global__ void __launch_bounds__(256)
@@ -400,7 +401,8 @@ __global__ void __launch_bounds__(256)
     const uint32_t row = blockIdx.x * 256 + threadIdx.x;
     const bool valid = row < p.n_rows;
     const double* col0 = p.matrix + row;
-    for (uint32_t s = warp; s < P; s += 8) {
+    (void)warp;
+    for (uint32_t s = 0; s < P; ++s) {
         const uint64_t a = p.offsets[s];
         const uint32_t len = s_len[s];
         bool ok = valid;
