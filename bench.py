@@ -193,7 +193,8 @@ def workload_config(t, args):
     return {"workload": f"{args.workload}: synthetic {s['rows']}x{s['cols']} "
                         f"({len(s['blocks'])} planted {s['blocks'][0][0]}x{s['blocks'][0][1]} trend blocks, "
                         f"seed {s['seed']}), reference GA novel batches (population 600)",
-            "rows": s["rows"], "cols": s["cols"], "series_per_step": len(t.batches[0][0]) - 1,
+            "rows": s["rows"], "cols": s["cols"],
+            "series_per_step": round(float(np.mean([len(b[0]) - 1 for b in t.batches])), 1),
             "eps": t.eps, "sigma": t.sigma, "l2": "flushed between timed steps (512 MB write)",
             "parallelism": f"rows sharded over {args.gpus} GPU(s)"}
 
@@ -224,7 +225,10 @@ def run_ours(args):
     else:
         ev = eb.Evaluator(values, devices=[local])
 
-    stream = torch.cuda.current_stream(dev)
+    # A dedicated stream: the kernels, the collectives and the timing events
+    # all run on it (events only see the stream they are recorded on).
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     st = stream.cuda_stream
     # Device-resident inputs: every batch's CBF in HBM.
     dev_batches = []
@@ -357,7 +361,9 @@ def run_ours(args):
                      "d2h_bytes_per_step": d2h} if e2e_val else None),
             "gpu_launches": args.steps * launches_per_step,
             "kernel_config": {"rows_per_tile": info.rows_per_tile, "stages": info.stages,
-                              "grid": info.grid, "sm_count": info.sm_count},
+                              "grid": info.grid, "sm_count": info.sm_count,
+                              "layout": ["fp64", "rank16x1", "rank16x2"][info.layout],
+                              "consumer_warps": info.consumer_warps},
             "parity": "counts and fitness bit-exact vs reference trace on every batch",
         }
         print(json.dumps(line), flush=True)

@@ -68,6 +68,8 @@ typedef struct ebic_ctx_info {
     int grid;             /* CTAs per count launch on shard 0 */
     size_t device_bytes;  /* matrix bytes resident on shard 0 */
     int sm_count;         /* SMs of shard 0's device */
+    int layout;           /* last count launch: 0 fp64 tile, 1/2 = exact rank tile (planes) */
+    int consumer_warps;   /* count-kernel consumer warps per CTA */
 } ebic_ctx_info;
 
 /* Library / device queries. */
@@ -127,8 +129,8 @@ double ebic_fitness_score(uint64_t match_count, size_t series_len, uint64_t sigm
 uint64_t ebic_default_sigma(size_t n_rows);
 
 /* Device-pointer variants (single-shard contexts) for callers that keep the
- * CBF in HBM and own the stream (cudaStream_t passed as void*; NULL = the
- * context's stream).  d_offsets: uint64[P+1]; d_cols: uint16[offsets[P]];
+ * CBF in HBM and own the stream (cudaStream_t passed as void*, used as is:
+ * NULL is the legacy default stream, as everywhere in CUDA).  d_offsets: uint64[P+1]; d_cols: uint16[offsets[P]];
  * total_len == offsets[P] (host-known).  d_counts_out: uint64[P] (partial
  * counts on a shard context).  d_fitness_out may be NULL; when non-NULL on a
  * whole-matrix context the fitness epilogue is fused into the count kernel.

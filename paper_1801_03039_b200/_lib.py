@@ -32,6 +32,8 @@ class CtxInfo(C.Structure):
         ("grid", C.c_int),
         ("device_bytes", C.c_size_t),
         ("sm_count", C.c_int),
+        ("layout", C.c_int),
+        ("consumer_warps", C.c_int),
     ]
 
 

@@ -96,15 +96,15 @@ class DeviceGuard {
     int prev_ = 0, dev_ = 0;
 };
 
-constexpr int kNCW = 16;       // consumer warps per count CTA
-constexpr size_t kMaxSeriesPerLaunch = 4096;
-constexpr size_t kMaxLenPerLaunch = 16384;
-constexpr int kThreads = (kNCW + 1) * 32;
+constexpr size_t kMaxSeriesPerLaunch = 2048;
+constexpr size_t kMaxLenPerLaunch = 8192;
 
 // Kernel configuration of the TMA count kernel for one shard.
 struct CountConfig {
+    int layout = 0;     // 0 = fp64 tile, 1 = rank (1 plane), 2 = rank (2 planes)
     int rpg = 0;        // rows per tile (0 = direct kernel)
     int rpl = 1;        // rows per lane
+    int ncw = 16;       // consumer warps per CTA
     int stages = 0;
     uint32_t box_cols = 0, n_boxes = 0, stage_bytes = 0;
 };
@@ -114,6 +114,17 @@ struct Tables {
     size_t n = 0;
     double* d_log = nullptr;
     double* d_exp = nullptr;
+};
+
+// Exact integer restatement of the matrix for one epsilon (RankWalker).
+struct RankLayout {
+    bool ok = false;
+    uint64_t eps_bits = 0;
+    int planes = 0;
+    uint16_t* d = nullptr;
+    CUtensorMap tmap;
+    bool tmap_ok = false;
+    uint64_t last_use = 0;
 };
 
 struct Shard {
@@ -139,6 +150,9 @@ struct Shard {
     unsigned char* h_pin = nullptr;
     size_t h_pin_cap = 0;
     Tables tables;
+    RankLayout ranks[2];
+    uint64_t rank_clock = 0;
+    int has_nan = -1;  // -1 unknown
     int last_grid = 0;
     CountConfig last_cfg;
 };
@@ -258,48 +272,71 @@ size_t tma_smem_bytes(const CountConfig& c, size_t P, size_t L) {
            count_meta_bytes((uint32_t)P, (uint32_t)L);
 }
 
-// Picks the row-tile height: the tallest tile (coalesced 128-byte column slices
-// at 16 rows) that still leaves a >= 3-deep TMA ring in shared memory.
-CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L) {
+// Fits a stage ring for a tile of `col_bytes` per column: the deepest ring
+// (>= min_stages, <= 4 unless forced) whose shared memory fits the budget.
+bool fit_ring(CountConfig& c, size_t n_cols, size_t col_bytes, size_t P, size_t L, size_t budget,
+              int min_stages, int want_stages) {
+    const uint32_t nb = (uint32_t)((n_cols + 255) / 256);
+    uint32_t bc = (uint32_t)((n_cols + nb - 1) / nb);
+    bc = (bc + 7) / 8 * 8;  // 128-byte aligned box destinations for every tile height
+    c.n_boxes = nb;
+    c.box_cols = bc;
+    const size_t sb = col_bytes * bc * nb;
+    if (sb >= (1u << 20)) return false;
+    c.stage_bytes = (uint32_t)sb;
+    int st = want_stages ? want_stages : kMaxStages;
+    for (; st >= min_stages; --st) {
+        c.stages = st;
+        if (tma_smem_bytes(c, P, L) <= budget) break;
+    }
+    if (st < min_stages) return false;
+    // Deep rings beyond 4 stages buy nothing once HBM is saturated.
+    if (!want_stages) c.stages = std::min(c.stages, 4);
+    return true;
+}
+
+// Chooses layout and tile.  Default: the exact rank layout (half the bytes of
+// fp64 per cell with eps != 0, a quarter with eps == 0; integer tests) when the
+// matrix is narrow enough for 16-bit ranks and the in-smem rank build; else the
+// fp64 tile with the tallest row tile (coalesced 128-byte column slices at 16
+// rows) that leaves a >= 3-deep TMA ring; else the unstaged direct kernel.
+CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int rank_planes) {
     CountConfig best;
     if (env_int("EBIC_FORCE_DIRECT", 0)) return best;
     const int want_rpg = env_int("EBIC_RPG", 0);
     const int want_rpl = env_int("EBIC_RPL", 0);
     const int want_stages = env_int("EBIC_STAGES", 0);
+    const int want_ncw = env_int("EBIC_NCW", 0);
     const size_t budget = (size_t)s.max_smem;
+    if (rank_planes) {
+        for (int min_stages : {3, 2}) {
+            CountConfig c;
+            c.layout = rank_planes;
+            c.rpg = rank_planes == 2 ? 32 : 64;
+            c.rpl = rank_planes == 2 ? 4 : 8;
+            c.ncw = want_ncw == 16 ? 16 : 32;
+            if (fit_ring(c, n_cols, 128, P, L, budget, min_stages, want_stages)) return c;
+        }
+    }
     for (int min_stages : {3, 2}) {
         for (int rpg : {16, 32, 8, 4}) {
             if (want_rpg && rpg != want_rpg) continue;
             CountConfig c;
             c.rpg = rpg;
-            c.rpl = want_rpl ? want_rpl : 1;
+            c.rpl = want_rpl ? want_rpl : 2;
             if (c.rpl > 1 && rpg < 4) c.rpl = 1;
-            const uint32_t nb = (uint32_t)((n_cols + 255) / 256);
-            uint32_t bc = (uint32_t)((n_cols + nb - 1) / nb);
-            bc = (bc + 7) / 8 * 8;  // 128-byte aligned box destinations for every rpg
-            c.n_boxes = nb;
-            c.box_cols = bc;
-            const size_t sb = size_t(rpg) * 8 * bc * nb;
-            if (sb >= (1u << 20)) continue;
-            c.stage_bytes = (uint32_t)sb;
-            int st = want_stages ? want_stages : kMaxStages;
-            for (; st >= min_stages; --st) {
-                c.stages = st;
-                if (tma_smem_bytes(c, P, L) <= budget) break;
-            }
-            if (st < min_stages) continue;
-            // Deep rings beyond 4 stages buy nothing once HBM is saturated.
-            if (!want_stages) c.stages = std::min(c.stages, 4);
-            return c;
+            c.ncw = (rpg == 16 && (want_ncw == 24 || want_ncw == 32)) ? want_ncw : (rpg == 16 ? 32 : 16);
+            if (want_ncw == 16) c.ncw = 16;
+            if (fit_ring(c, n_cols, size_t(rpg) * 8, P, L, budget, min_stages, want_stages)) return c;
         }
     }
     return best;  // rpg == 0 -> direct kernel
 }
 
-template <int RPG, int RPL, bool E0>
+template <class W, int NCW>
 void launch_tma_t(const CUtensorMap& tm, const CountParams& p, int grid, size_t smem,
                   cudaStream_t st) {
-    auto k = count_tma_kernel<RPG, RPL, kNCW, E0>;
+    auto k = count_tma_kernel<W, NCW>;
     // The attribute is per function and device; set it only when it grows so
     // the per-generation launch path makes no extra driver calls.
     static int smem_set[64] = {0};
@@ -309,30 +346,122 @@ void launch_tma_t(const CUtensorMap& tm, const CountParams& p, int grid, size_t 
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         if (dev >= 0 && dev < 64) smem_set[dev] = (int)smem;
     }
-    k<<<grid, kThreads, smem, st>>>(tm, p);
+    k<<<grid, (NCW + 1) * 32, smem, st>>>(tm, p);
 }
 
-template <int RPG, int RPL>
-void launch_tma_e(bool e0, const CUtensorMap& tm, const CountParams& p, int grid, size_t smem,
-                  cudaStream_t st) {
-    if (e0) launch_tma_t<RPG, RPL, true>(tm, p, grid, smem, st);
-    else launch_tma_t<RPG, RPL, false>(tm, p, grid, smem, st);
+template <int RPG, int RPL, int NCW>
+void launch_f64(bool e0, const CUtensorMap& tm, const CountParams& p, int grid, size_t smem,
+                cudaStream_t st) {
+    if (e0) launch_tma_t<F64Walker<RPG, RPL, true>, NCW>(tm, p, grid, smem, st);
+    else launch_tma_t<F64Walker<RPG, RPL, false>, NCW>(tm, p, grid, smem, st);
 }
 
 void launch_tma(const CountConfig& c, bool e0, const CUtensorMap& tm, const CountParams& p,
                 int grid, size_t smem, cudaStream_t st) {
-    switch (c.rpg * 10 + c.rpl) {
-        case 321: launch_tma_e<32, 1>(e0, tm, p, grid, smem, st); break;
-        case 322: launch_tma_e<32, 2>(e0, tm, p, grid, smem, st); break;
-        case 161: launch_tma_e<16, 1>(e0, tm, p, grid, smem, st); break;
-        case 162: launch_tma_e<16, 2>(e0, tm, p, grid, smem, st); break;
-        case 81: launch_tma_e<8, 1>(e0, tm, p, grid, smem, st); break;
-        case 82: launch_tma_e<8, 2>(e0, tm, p, grid, smem, st); break;
-        case 41: launch_tma_e<4, 1>(e0, tm, p, grid, smem, st); break;
-        case 42: launch_tma_e<4, 2>(e0, tm, p, grid, smem, st); break;
+    if (c.layout) {
+        const bool n16 = c.ncw == 16;
+        if (c.layout == 2) {
+            if (n16) launch_tma_t<RankWalker<2>, 16>(tm, p, grid, smem, st);
+            else launch_tma_t<RankWalker<2>, 31>(tm, p, grid, smem, st);
+        } else {
+            if (n16) launch_tma_t<RankWalker<1>, 16>(tm, p, grid, smem, st);
+            else launch_tma_t<RankWalker<1>, 31>(tm, p, grid, smem, st);
+        }
+        CK(cudaGetLastError());
+        return;
+    }
+    switch (c.rpg * 1000 + c.rpl * 100 + c.ncw) {
+        case 32116: launch_f64<32, 1, 16>(e0, tm, p, grid, smem, st); break;
+        case 32216: launch_f64<32, 2, 16>(e0, tm, p, grid, smem, st); break;
+        case 16116: launch_f64<16, 1, 16>(e0, tm, p, grid, smem, st); break;
+        case 16216: launch_f64<16, 2, 16>(e0, tm, p, grid, smem, st); break;
+        case 16124: launch_f64<16, 1, 24>(e0, tm, p, grid, smem, st); break;
+        case 16224: launch_f64<16, 2, 24>(e0, tm, p, grid, smem, st); break;
+        case 16132: launch_f64<16, 1, 31>(e0, tm, p, grid, smem, st); break;
+        case 16232: launch_f64<16, 2, 31>(e0, tm, p, grid, smem, st); break;
+        case 8116: launch_f64<8, 1, 16>(e0, tm, p, grid, smem, st); break;
+        case 8216: launch_f64<8, 2, 16>(e0, tm, p, grid, smem, st); break;
+        case 4116: launch_f64<4, 1, 16>(e0, tm, p, grid, smem, st); break;
+        case 4216: launch_f64<4, 2, 16>(e0, tm, p, grid, smem, st); break;
         default: fail(EBIC_ERR_RUNTIME, "unsupported count-kernel configuration");
     }
     CK(cudaGetLastError());
+}
+
+constexpr size_t kRankMaxCols = 2048;  // 2C keys sorted in shared memory per row
+
+uint64_t eps_key(double eps) {
+    if (eps == 0.0) eps = 0.0;  // -0.0 and +0.0 give identical predicates
+    uint64_t b;
+    std::memcpy(&b, &eps, sizeof b);
+    return b;
+}
+
+// The exact rank layout of this shard for `eps` (built on first use, two
+// epsilons cached), or nullptr when the fp64 tile must be used.
+RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
+    if (n_cols > kRankMaxCols || env_int("EBIC_LAYOUT_F64", 0)) return nullptr;
+    const uint64_t key = eps_key(eps);
+    for (RankLayout& rl : s.ranks)
+        if (rl.ok && rl.eps_bits == key) {
+            rl.last_use = ++s.rank_clock;
+            return &rl;
+        }
+    if (s.has_nan < 0) {
+        int* d_flag = nullptr;
+        CK(cudaMalloc(&d_flag, sizeof(int)));
+        CK(cudaMemsetAsync(d_flag, 0, sizeof(int), s.stream));
+        has_nan_kernel<<<s.sm_count * 4, 256, 0, s.stream>>>(s.d_mat, s.ld, s.rows, s.ld * n_cols, d_flag);
+        CK(cudaGetLastError());
+        int h = 0;
+        CK(cudaMemcpyAsync(&h, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s.stream));
+        CK(cudaStreamSynchronize(s.stream));
+        CK(cudaFree(d_flag));
+        s.has_nan = h;
+    }
+    RankLayout& rl = s.ranks[0].last_use <= s.ranks[1].last_use ? s.ranks[0] : s.ranks[1];
+    const int planes = (eps == 0.0 && !s.has_nan) ? 1 : 2;
+    if (rl.d && rl.planes != planes) {
+        CK(cudaFree(rl.d));
+        rl.d = nullptr;
+    }
+    if (!rl.d) CK(cudaMalloc(&rl.d, size_t(planes) * s.ld * n_cols * sizeof(uint16_t)));
+    rl.ok = false;
+    rl.tmap_ok = false;
+    rl.planes = planes;
+    rl.eps_bits = key;
+    uint32_t Kp = 1;
+    while (Kp < planes * n_cols) Kp <<= 1;
+    const size_t smem = size_t(Kp) * 16 + 32 * 4 + 64;
+    if (planes == 2) {
+        CK(cudaFuncSetAttribute(rank_build_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        rank_build_kernel<2><<<(unsigned)s.ld, 256, smem, s.stream>>>(s.d_mat, (uint32_t)s.ld, (uint32_t)s.rows, (uint32_t)n_cols, eps, Kp, rl.d);
+    } else {
+        CK(cudaFuncSetAttribute(rank_build_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        rank_build_kernel<1><<<(unsigned)s.ld, 256, smem, s.stream>>>(s.d_mat, (uint32_t)s.ld, (uint32_t)s.rows, (uint32_t)n_cols, eps, Kp, rl.d);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s.stream));
+    rl.ok = true;
+    rl.last_use = ++s.rank_clock;
+    return &rl;
+}
+
+const CUtensorMap& rank_tensor_map(RankLayout& rl, const Shard& s, size_t n_cols, const CountConfig& cfg) {
+    if (!rl.tmap_ok) {
+        cuuint64_t dims[2] = {(cuuint64_t)(s.ld * rl.planes), (cuuint64_t)n_cols};
+        cuuint64_t strides[1] = {(cuuint64_t)(s.ld * rl.planes * sizeof(uint16_t))};
+        cuuint32_t box[2] = {64u, cfg.box_cols};  // 128 bytes per column slice
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = tensor_map_encoder()(&rl.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, rl.d, dims,
+                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_NONE,
+                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) fail(EBIC_ERR_CUDA, "cuTensorMapEncodeTiled (ranks) failed (" + std::to_string((int)r) + ")");
+        rl.tmap_ok = true;
+    }
+    return rl.tmap;
 }
 
 // Host-built Eq. 1 tables (same glibc log/exp2 as fitness.hpp:129,131).
@@ -389,7 +518,8 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         p.expt = t.d_exp;
     }
     const bool e0 = (eps == 0.0);
-    CountConfig c = choose_config(s, ctx.n_cols, P, L);
+    RankLayout* rl = ensure_ranks(s, ctx.n_cols, eps);
+    CountConfig c = choose_config(s, ctx.n_cols, P, L, rl ? rl->planes : 0);
     if (c.rpg) {
         p.box_cols = c.box_cols;
         p.n_boxes = c.n_boxes;
@@ -402,7 +532,8 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         if (g_env > 0) grid = std::min<int>(g_env, (int)p.n_tiles);
         s.last_grid = grid;
         s.last_cfg = c;
-        launch_tma(c, e0, tensor_map(s, ctx.n_cols, c), p, grid, smem, st);
+        const CUtensorMap& tm = c.layout ? rank_tensor_map(*rl, s, ctx.n_cols, c) : tensor_map(s, ctx.n_cols, c);
+        launch_tma(c, e0, tm, p, grid, smem, st);
     } else {
         const size_t smem = 8 * P + 16;
         if (smem > (size_t)s.max_smem) fail(EBIC_ERR_INVALID_ARGUMENT, "population too large for one launch");
@@ -558,6 +689,7 @@ void free_shard(Shard& s) {
     if (s.h_pin) cudaFreeHost(s.h_pin);
     cudaFree(s.tables.d_log);
     cudaFree(s.tables.d_exp);
+    for (RankLayout& rl : s.ranks) cudaFree(rl.d);
     if (s.stream) cudaStreamDestroy(s.stream);
 }
 
@@ -690,6 +822,8 @@ int ebic_ctx_get_info(const ebic_ctx* ctx, ebic_ctx_info* info) {
         info->grid = s.last_grid;
         info->device_bytes = s.ld * ctx->n_cols * sizeof(double);
         info->sm_count = s.sm_count;
+        info->layout = s.last_cfg.layout;
+        info->consumer_warps = s.last_cfg.ncw == 32 ? 31 : s.last_cfg.ncw;
     });
 }
 
@@ -738,7 +872,7 @@ int ebic_count_matches_device(ebic_ctx* ctx, const uint64_t* d_offsets, const ui
         if (d_fitness_out && !whole) fail(EBIC_ERR_INVALID_ARGUMENT, "fitness needs reduced counts on a shard context");
         if (n_series > kMaxSeriesPerLaunch || total_len > kMaxLenPerLaunch)
             fail(EBIC_ERR_INVALID_ARGUMENT, "device batch exceeds 4096 series / 16384 columns; split it");
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s.stream;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream
         launch_count(*ctx, s, d_offsets, d_cols, n_series, total_len, eps, d_counts_out, d_fitness_out,
                      sigma, st);
     });
@@ -751,7 +885,7 @@ int ebic_fitness_device(ebic_ctx* ctx, const uint64_t* d_counts, const uint64_t*
         DeviceGuard g(s.device);
         if (n_series == 0) return;
         const Tables& t = ensure_tables(s, sigma, ctx->total_rows);
-        cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : s.stream;
+        cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream
         fitness_kernel<<<(unsigned)((n_series + 255) / 256), 256, 0, st>>>(
             d_counts, d_offsets, (uint32_t)n_series, sigma, t.d_log, t.d_exp, d_fitness_out);
         CK(cudaGetLastError());

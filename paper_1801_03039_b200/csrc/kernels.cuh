@@ -147,76 +147,167 @@ struct CountParams {
     uint32_t ld;                           // leading dimension (direct kernel only)
 };
 
-// Smem layout: [stages * stage_bytes][mbar full/empty][meta]; meta =
-//   s_start  u32[P]  first column position of series (in s_cols)
-//   s_len    u32[P]
-//   s_order  u32[P]  series ids sorted by length bucket
-//   s_cnt    u32[P]  per-CTA match counts
-//   s_cols   u16[total_len]
-//   s_hist   u32[kLenBuckets]
+// Shared-memory work list of one count launch (P series, L column entries):
+//   s_sl     u32[P]   slot -> series id (slots are length-sorted)
+//   s_slen   u32[P]   slot -> series length
+//   s_sstart u32[P]   slot -> first entry in s_pcols (multiple of 8)
+//   s_cnt    u32[P]   slot -> per-CTA match count
+//   s_rel    u32[P+1] series offsets relative to offsets[0] (prologue scratch)
+//   s_pcols  u16[L + 7P] column lists, each padded to a multiple of 8 entries
+//                     (16-byte aligned: one LDS.128 fetches 8 column indices)
+//   s_raw    u16[L]   the launch's column indices (prologue scratch)
+//   s_hist   u32[kLenBuckets], s_wsum u32[32]
 __host__ __device__ inline size_t count_meta_bytes(uint32_t P, uint32_t total_len) {
-    size_t b = 4ull * P * 4 + 2ull * total_len;
+    size_t b = 16ull * P + 4ull * (P + 1);
     b = (b + 15) & ~size_t(15);
-    return b + 4ull * kLenBuckets + 16;
+    b += 2ull * (total_len + 7ull * P) + 16;
+    b = (b + 15) & ~size_t(15);
+    b += 2ull * total_len + 16;
+    b = (b + 15) & ~size_t(15);
+    return b + 4ull * kLenBuckets + 4ull * 32 + 16;
 }
 
-// Cooperative (all `nthreads` threads of the group) construction of the work
-// list: series lengths, a length-bucketed order (so the lane groups of one warp
-// walk equally long series), zeroed counters and the column list in smem.
-__device__ __forceinline__ void build_work_list(const CountParams& p, uint32_t* s_start,
-                                                uint32_t* s_len, uint32_t* s_order,
-                                                uint32_t* s_cnt, uint16_t* s_cols, uint32_t* s_hist,
-                                                int tid, int nthreads, int bar_id) {
-    const uint32_t P = p.n_series;
-    for (int b = tid; b < kLenBuckets; b += nthreads) s_hist[b] = 0;
-    named_bar_sync(bar_id, nthreads);
-    // A launch may cover a slice of a larger population: positions are taken
-    // relative to offsets[0].
-    const uint64_t base = p.offsets[0];
-    for (uint32_t s = tid; s < P; s += nthreads) {
-        const uint64_t a = p.offsets[s], e = p.offsets[s + 1];
-        const uint32_t len = static_cast<uint32_t>(e - a);
-        s_start[s] = static_cast<uint32_t>(a - base);
-        s_len[s] = len;
-        s_cnt[s] = 0;
-        atomicAdd(&s_hist[len < kLenBuckets ? len : kLenBuckets - 1], 1u);
+struct WorkList {
+    uint32_t* sl;
+    uint32_t* slen;
+    uint32_t* sstart;
+    uint32_t* cnt;
+    uint32_t* rel;
+    uint16_t* pcols;
+    uint16_t* raw;
+    uint32_t* hist;
+    uint32_t* wsum;
+};
+
+__device__ __forceinline__ unsigned char* align16(unsigned char* base, size_t off) {
+    return base + ((off + 15) & ~size_t(15));
+}
+
+// Carves the work list out of shared memory starting at `p` (16-byte aligned).
+// Pointer arithmetic on the shared window only (keeps LDS/STS addressing).
+__device__ __forceinline__ WorkList carve_work_list(unsigned char* p, uint32_t P, uint32_t L) {
+    WorkList w;
+    w.sl = reinterpret_cast<uint32_t*>(p);
+    w.slen = w.sl + P;
+    w.sstart = w.slen + P;
+    w.cnt = w.sstart + P;
+    w.rel = w.cnt + P;
+    size_t off = 16ull * P + 4ull * (P + 1);
+    unsigned char* q = align16(p, off);
+    w.pcols = reinterpret_cast<uint16_t*>(q);
+    q = align16(q, 2ull * (L + 7ull * P) + 16);
+    w.raw = reinterpret_cast<uint16_t*>(q);
+    q = align16(q, 2ull * L + 16);
+    w.hist = reinterpret_cast<uint32_t*>(q);
+    w.wsum = w.hist + kLenBuckets;
+    return w;
+}
+
+// Exclusive scan over P items by `nthreads` threads (blocked partition).
+// vals(g) -> item g; writes out[g]; all threads of the group participate.
+template <class F>
+__device__ __forceinline__ void block_exclusive_scan(uint32_t P, F vals, uint32_t* out,
+                                                     uint32_t* wsum, int tid, int nthreads,
+                                                     int bar_id) {
+    const uint32_t per = (P + nthreads - 1) / nthreads;
+    const uint32_t lo = min(P, tid * per), hi = min(P, lo + per);
+    uint32_t local = 0;
+    for (uint32_t g = lo; g < hi; ++g) local += vals(g);
+    const int lane = tid & 31, warp = tid >> 5;
+    uint32_t incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
     }
-    for (uint32_t i = tid; i < p.total_len; i += nthreads) s_cols[i] = p.cols[base + i];
+    if (lane == 31) wsum[warp] = incl;
     named_bar_sync(bar_id, nthreads);
-    if (tid < 32) {  // exclusive scan of 64 buckets by one warp
-        uint32_t a = s_hist[tid], b = s_hist[tid + 32];
+    if (warp == 0) {
+        const int nw = nthreads >> 5;
+        uint32_t x = lane < nw ? wsum[lane] : 0u, xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += y;
+        }
+        if (lane < nw) wsum[lane] = xi - x;
+    }
+    named_bar_sync(bar_id, nthreads);
+    uint32_t run = wsum[warp] + incl - local;
+    for (uint32_t g = lo; g < hi; ++g) {
+        out[g] = run;
+        run += vals(g);
+    }
+}
+
+// Cooperative construction of the work list by `nthreads` threads.  One
+// round trip to global memory (offsets + column indices, coalesced), then
+// shared memory only: series are bucket-sorted by length (so the lane groups
+// of one warp walk equally long series) and each series' columns are copied
+// to a padded, 16-byte aligned slot (pad entries hold column 0, a valid
+// address).  Runs while the producer's first TMA stages are in flight.
+__device__ __forceinline__ void build_work_list(const CountParams& p, const WorkList& w, int tid,
+                                                int nthreads, int bar_id) {
+    const uint32_t P = p.n_series, L = p.total_len;
+    // A launch may cover a slice of a larger population: column positions are
+    // taken relative to offsets[0].
+    const uint64_t base = p.offsets[0];
+    for (uint32_t s = tid; s <= P; s += nthreads) w.rel[s] = static_cast<uint32_t>(p.offsets[s] - base);
+    const uint16_t* gcols = p.cols + base;
+    for (uint32_t i = tid; i < L; i += nthreads) w.raw[i] = gcols[i];
+    for (int b = tid; b < kLenBuckets; b += nthreads) w.hist[b] = 0;
+    named_bar_sync(bar_id, nthreads);
+    for (uint32_t s = tid; s < P; s += nthreads) {
+        const uint32_t len = w.rel[s + 1] - w.rel[s];
+        atomicAdd(&w.hist[len < kLenBuckets ? len : kLenBuckets - 1], 1u);
+    }
+    named_bar_sync(bar_id, nthreads);
+    if (tid < 32) {  // exclusive scan of the 64 bucket sizes by one warp
+        const uint32_t a = w.hist[tid], b = w.hist[tid + 32];
         uint32_t x = a;
         for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (tid >= o) x += y;
         }
         const uint32_t total_a = __shfl_sync(0xffffffffu, x, 31);
         uint32_t z = b;
         for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+            const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
             if (tid >= o) z += y;
         }
-        s_hist[tid] = x - a;
-        s_hist[tid + 32] = total_a + z - b;
+        w.hist[tid] = x - a;
+        w.hist[tid + 32] = total_a + z - b;
     }
     named_bar_sync(bar_id, nthreads);
     for (uint32_t s = tid; s < P; s += nthreads) {
-        const uint32_t len = s_len[s];
-        const uint32_t pos = atomicAdd(&s_hist[len < kLenBuckets ? len : kLenBuckets - 1], 1u);
-        s_order[pos] = s;
+        const uint32_t len = w.rel[s + 1] - w.rel[s];
+        const uint32_t g = atomicAdd(&w.hist[len < kLenBuckets ? len : kLenBuckets - 1], 1u);
+        w.sl[g] = s;
+        w.slen[g] = len;
+        w.cnt[g] = 0;
+    }
+    named_bar_sync(bar_id, nthreads);
+    block_exclusive_scan(P, [&](uint32_t g) { return (w.slen[g] + 7u) & ~7u; }, w.sstart, w.wsum,
+                         tid, nthreads, bar_id);
+    named_bar_sync(bar_id, nthreads);
+    for (uint32_t g = tid; g < P; g += nthreads) {
+        const uint32_t len = w.slen[g], st = w.sstart[g];
+        const uint16_t* src = w.raw + w.rel[w.sl[g]];
+        const uint32_t padded = (len + 7u) & ~7u;
+        for (uint32_t i = 0; i < padded; ++i) w.pcols[st + i] = i < len ? src[i] : 0;
     }
     named_bar_sync(bar_id, nthreads);
 }
 
-// Grid-wide reduction tail shared by both count kernels: per-CTA counts are
+// Grid-wide reduction tail shared by the count kernels: per-CTA counts are
 // added to the global accumulator; the last CTA to arrive publishes the final
 // counts (and Eq. 1 fitness when tables are given) and re-zeroes the
-// accumulator and arrival counter for the next launch.
+// accumulator and arrival counter for the next launch.  `slot_series` maps a
+// counter slot to its series id (nullptr = identity).
 __device__ __forceinline__ void count_epilogue(const CountParams& p, const uint32_t* s_cnt,
-                                               const uint32_t* s_len) {
+                                               const uint32_t* slot_series) {
     const uint32_t P = p.n_series;
-    for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
-        const uint32_t c = s_cnt[s];
+    for (uint32_t g = threadIdx.x; g < P; g += blockDim.x) {
+        const uint32_t c = s_cnt[g];
+        const uint32_t s = slot_series ? slot_series[g] : g;
         if (c) atomicAdd(&p.acc[s], static_cast<unsigned long long>(c));
     }
     __threadfence();
@@ -229,52 +320,295 @@ __device__ __forceinline__ void count_epilogue(const CountParams& p, const uint3
     for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
         const uint64_t c = atomicExch(&p.acc[s], 0ull);
         p.counts_out[s] = c;
-        if (p.fitness_out) p.fitness_out[s] = fitness_from_tables(c, s_len[s], p.sigma, p.logt, p.expt);
+        if (p.fitness_out)
+            p.fitness_out[s] = fitness_from_tables(c, p.offsets[s + 1] - p.offsets[s], p.sigma,
+                                                   p.logt, p.expt);
     }
     if (threadIdx.x == 0) *p.done = 0u;
 }
 
 // ---------------------------------------------------------------------------
+// Series walkers over a staged fp64 tile: [col][RPG] doubles, one lane = RPL
+// consecutive rows at byte offset gl*RPL*8.  Result: per-lane bit mask of
+// matching rows (bit k = row k of the lane).  Branch-free AND over every
+// adjacent pair: the same boolean as the reference's early-exit loop.
+// ---------------------------------------------------------------------------
+template <int RPG, int RPL, bool kEpsZero>
+struct F64Walker {
+    static constexpr int kShift = (RPG == 32) ? 8 : (RPG == 16) ? 7 : (RPG == 8) ? 6 : (RPG == 4) ? 5 : 4;
+    static_assert((1 << kShift) == RPG * 8, "RPG must be a power of two in [2,32]");
+    static constexpr uint32_t kAll = (1u << RPL) - 1u;
+    // tile geometry (see count_tma_kernel)
+    static constexpr int kRowsPerTile = RPG;
+    static constexpr int kRowsPerLane = RPL;
+    static constexpr int kLaneBytes = RPL * 8;
+    static constexpr int kColBytes = RPG * 8;      // one column of a staged tile
+    static constexpr int kDim0PerTile = RPG;       // TMA dim-0 extent of a tile (fp64 elements)
+    using Mask = uint32_t;
+    __device__ __forceinline__ static Mask valid(uint32_t row0, uint32_t n_rows) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) m |= (row0 + k < n_rows) ? (1u << k) : 0u;
+        return m;
+    }
+
+    __device__ __forceinline__ static uint32_t col_at(const uint32_t* w, int i) {
+        const uint32_t x = w[i >> 1];
+        return (i & 1) ? (x >> 16) : (x & 0xffffu);
+    }
+
+    // All lane groups of the warp walk series of exactly L columns.
+    template <int L>
+    __device__ __forceinline__ static uint32_t walk_fixed(const unsigned char* base,
+                                                          const uint16_t* pc, double eps) {
+        uint32_t w[8];
+        const uint4 q0 = *reinterpret_cast<const uint4*>(pc);
+        w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
+        if (L > 8) {
+            const uint4 q1 = *reinterpret_cast<const uint4*>(pc + 8);
+            w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+        }
+        if (RPL == 1) {
+            double prev = *reinterpret_cast<const double*>(base + (col_at(w, 0) << kShift));
+            bool ok = true;
+#pragma unroll
+            for (int i = 1; i < L; ++i) {
+                const double cur = *reinterpret_cast<const double*>(base + (col_at(w, i) << kShift));
+                ok = ok & step_ok<kEpsZero>(prev, cur, eps);
+                prev = cur;
+            }
+            return ok ? 1u : 0u;
+        } else {
+            double2 prev = *reinterpret_cast<const double2*>(base + (col_at(w, 0) << kShift));
+            bool a = true, b = true;
+#pragma unroll
+            for (int i = 1; i < L; ++i) {
+                const double2 cur = *reinterpret_cast<const double2*>(base + (col_at(w, i) << kShift));
+                a = a & step_ok<kEpsZero>(prev.x, cur.x, eps);
+                b = b & step_ok<kEpsZero>(prev.y, cur.y, eps);
+                prev = cur;
+            }
+            return (a ? 1u : 0u) | (b ? 2u : 0u);
+        }
+    }
+
+    // Any length, per-lane trip count (mixed-length warps, long series).
+    __device__ __forceinline__ static uint32_t walk_any(const unsigned char* base,
+                                                        const uint16_t* pc, uint32_t len,
+                                                        double eps) {
+        if (len <= 1) return kAll;  // no adjacent pair: the row matches (fitness.hpp:80-90)
+        if (RPL == 1) {
+            double prev = *reinterpret_cast<const double*>(base + (uint32_t(pc[0]) << kShift));
+            bool ok = true;
+            for (uint32_t i = 1; i < len; ++i) {
+                const double cur = *reinterpret_cast<const double*>(base + (uint32_t(pc[i]) << kShift));
+                ok = ok & step_ok<kEpsZero>(prev, cur, eps);
+                prev = cur;
+            }
+            return ok ? 1u : 0u;
+        } else {
+            double2 prev = *reinterpret_cast<const double2*>(base + (uint32_t(pc[0]) << kShift));
+            bool a = true, b = true;
+            for (uint32_t i = 1; i < len; ++i) {
+                const double2 cur = *reinterpret_cast<const double2*>(base + (uint32_t(pc[i]) << kShift));
+                a = a & step_ok<kEpsZero>(prev.x, cur.x, eps);
+                b = b & step_ok<kEpsZero>(prev.y, cur.y, eps);
+                prev = cur;
+            }
+            return (a ? 1u : 0u) | (b ? 2u : 0u);
+        }
+    }
+
+    __device__ __forceinline__ static uint32_t count(const unsigned char* base, const uint16_t* pc,
+                                                     uint32_t len, bool uniform, double eps,
+                                                     Mask vm) {
+        return __popc(walk(base, pc, len, uniform, eps) & vm);
+    }
+
+    __device__ __forceinline__ static uint32_t walk(const unsigned char* base, const uint16_t* pc,
+                                                    uint32_t len, bool uniform, double eps) {
+        if (uniform) {
+            switch (len) {
+                case 2: return walk_fixed<2>(base, pc, eps);
+                case 3: return walk_fixed<3>(base, pc, eps);
+                case 4: return walk_fixed<4>(base, pc, eps);
+                case 5: return walk_fixed<5>(base, pc, eps);
+                case 6: return walk_fixed<6>(base, pc, eps);
+                case 7: return walk_fixed<7>(base, pc, eps);
+                case 8: return walk_fixed<8>(base, pc, eps);
+                case 9: return walk_fixed<9>(base, pc, eps);
+                case 10: return walk_fixed<10>(base, pc, eps);
+                case 11: return walk_fixed<11>(base, pc, eps);
+                case 12: return walk_fixed<12>(base, pc, eps);
+                default: break;
+            }
+        }
+        return walk_any(base, pc, len, eps);
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Series walker over a staged RANK tile (exact integer restatement of the fp64
+// predicate; built by rank_build_kernel).  For every row, each cell's value v
+// and its slack-shifted value fl(v + eps) are replaced by their dense ranks
+// among the row's values {v_j} u {fl(v_j + eps)}; then
+//     v_a < fl(v_b + eps)   <=>   lo(a) < hi(b)
+// exactly (ranks preserve strict order; ties share a rank; NaN maps to
+// sentinels that fail every test, as NaN compares false).  Ranks are stored
+// with bit 15 set (r' = r | 0x8000, r <= 0x7fff), two rows per 32-bit word;
+// for one word pair the test of both rows is one IADD3 + one LOP3:
+//     ok &= hi'(cur) - lo'(prev) + 0x7fff7fff      (bit 15 / bit 31 = row test)
+// since each 16-bit lane of the sum is hi - lo + 0x7fff in [0, 0xfffc] (no
+// carry between lanes) and has bit 15 set iff hi > lo.
+//   PLANES == 2 (eps != 0 or NaN present): a column slice holds, per 4 rows,
+//     lo'[4] then hi'[4] (16 bytes); a lane owns 4 rows (one LDS.128).
+//   PLANES == 1 (eps == 0, no NaN): lo == hi, one u16 per cell; a lane owns
+//     8 rows (one LDS.128).
+// Tile: 128 bytes per column (32 rows x 2 planes, or 64 rows x 1 plane).
+// ---------------------------------------------------------------------------
+template <int PLANES>
+struct RankWalker {
+    static constexpr int kRowsPerLane = PLANES == 2 ? 4 : 8;
+    static constexpr int kRowsPerTile = PLANES == 2 ? 32 : 64;
+    static constexpr int kLaneBytes = 16;
+    static constexpr int kColBytes = 128;
+    static constexpr int kShift = 7;
+    static constexpr int kDim0PerTile = kRowsPerTile * PLANES;  // u16 elements
+    static constexpr int kWords = kRowsPerLane / 2;           // ok words per lane
+    struct Mask {
+        uint32_t m[kWords];
+    };
+    __device__ __forceinline__ static Mask valid(uint32_t row0, uint32_t n_rows) {
+        Mask v;
+#pragma unroll
+        for (int k = 0; k < kWords; ++k)
+            v.m[k] = ((row0 + 2 * k < n_rows) ? 0x8000u : 0u) |
+                     ((row0 + 2 * k + 1 < n_rows) ? 0x80000000u : 0u);
+        return v;
+    }
+    __device__ __forceinline__ static uint32_t col_at(const uint32_t* w, int i) {
+        const uint32_t x = w[i >> 1];
+        return (i & 1) ? (x >> 16) : (x & 0xffffu);
+    }
+    __device__ __forceinline__ static uint4 ld(const unsigned char* base, uint32_t col) {
+        return *reinterpret_cast<const uint4*>(base + (col << kShift));
+    }
+    // One adjacent pair: ok[k] accumulates bit 15/31 per row.
+    __device__ __forceinline__ static void step(uint32_t* ok, const uint4& prev, const uint4& cur) {
+        if (PLANES == 2) {
+            ok[0] &= cur.z - prev.x + 0x7fff7fffu;
+            ok[1] &= cur.w - prev.y + 0x7fff7fffu;
+        } else {
+            ok[0] &= cur.x - prev.x + 0x7fff7fffu;
+            ok[1] &= cur.y - prev.y + 0x7fff7fffu;
+            ok[2] &= cur.z - prev.z + 0x7fff7fffu;
+            ok[3] &= cur.w - prev.w + 0x7fff7fffu;
+        }
+    }
+    __device__ __forceinline__ static uint32_t tally(const uint32_t* ok, const Mask& vm) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int k = 0; k < kWords; ++k) c += __popc(ok[k] & vm.m[k]);
+        return c;
+    }
+    template <int L>
+    __device__ __forceinline__ static uint32_t count_fixed(const unsigned char* base,
+                                                           const uint16_t* pc, const Mask& vm) {
+        uint32_t w[8];
+        const uint4 q0 = *reinterpret_cast<const uint4*>(pc);
+        w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
+        if (L > 8) {
+            const uint4 q1 = *reinterpret_cast<const uint4*>(pc + 8);
+            w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+        }
+        uint32_t ok[kWords];
+#pragma unroll
+        for (int k = 0; k < kWords; ++k) ok[k] = 0xffffffffu;
+        uint4 prev = ld(base, col_at(w, 0));
+#pragma unroll
+        for (int i = 1; i < L; ++i) {
+            const uint4 cur = ld(base, col_at(w, i));
+            step(ok, prev, cur);
+            prev = cur;
+        }
+        return tally(ok, vm);
+    }
+    __device__ __forceinline__ static uint32_t count_any(const unsigned char* base,
+                                                         const uint16_t* pc, uint32_t len,
+                                                         const Mask& vm) {
+        uint32_t ok[kWords];
+#pragma unroll
+        for (int k = 0; k < kWords; ++k) ok[k] = 0xffffffffu;
+        if (len > 1) {  // len <= 1: no adjacent pair, every row matches (fitness.hpp:80-90)
+            uint4 prev = ld(base, pc[0]);
+            for (uint32_t i = 1; i < len; ++i) {
+                const uint4 cur = ld(base, pc[i]);
+                step(ok, prev, cur);
+                prev = cur;
+            }
+        }
+        return tally(ok, vm);
+    }
+    __device__ __forceinline__ static uint32_t count(const unsigned char* base, const uint16_t* pc,
+                                                     uint32_t len, bool uniform, double,
+                                                     const Mask& vm) {
+        if (uniform) {
+            switch (len) {
+                case 2: return count_fixed<2>(base, pc, vm);
+                case 3: return count_fixed<3>(base, pc, vm);
+                case 4: return count_fixed<4>(base, pc, vm);
+                case 5: return count_fixed<5>(base, pc, vm);
+                case 6: return count_fixed<6>(base, pc, vm);
+                case 7: return count_fixed<7>(base, pc, vm);
+                case 8: return count_fixed<8>(base, pc, vm);
+                case 9: return count_fixed<9>(base, pc, vm);
+                case 10: return count_fixed<10>(base, pc, vm);
+                case 11: return count_fixed<11>(base, pc, vm);
+                case 12: return count_fixed<12>(base, pc, vm);
+                default: break;
+            }
+        }
+        return count_any(base, pc, len, vm);
+    }
+};
+
+// ---------------------------------------------------------------------------
 // K1: TMA-staged count kernel.
 //
-// Persistent CTAs (grid <= SMs x occupancy) walk row tiles tile = blockIdx.x,
+// Persistent CTAs (grid <= SMs) walk row tiles tile = blockIdx.x,
 // blockIdx.x + gridDim.x, ...  A tile is RPG rows x all n_cols columns of the
 // column-major matrix, brought into shared memory by one producer warp with 2D
 // TMA boxes (RPG rows x box_cols columns, landing as [col][RPG] doubles) into a
-// `stages`-deep mbarrier ring.  NCW consumer warps then evaluate EVERY series of
-// the population against the staged tile, so the matrix is read from HBM once
-// per launch.  A warp is split into lane groups of RPG/RPL lanes; each group
-// walks one series, each lane RPL adjacent rows (RPL = 2 -> 16-byte LDS.128).
-// The walk is branch-free (AND of every adjacent test; identical boolean to the
-// reference's early exit), groups of a warp take consecutive entries of the
-// length-sorted order so they rarely diverge, and row hits are counted with
-// __ballot_sync + __popc into per-CTA shared counters.
+// `stages`-deep mbarrier ring, so the matrix is read from HBM exactly once per
+// launch.  NCW consumer warps evaluate EVERY series of the population against
+// the staged tile.  A warp is split into GW lane groups of RPG/RPL lanes; a
+// group walks one series, a lane RPL adjacent rows (RPL = 2: 16-byte LDS.128).
+// Groups of one warp take consecutive slots of the length-sorted work list;
+// when their lengths agree (the common case) the walk is fully unrolled with
+// 8 column indices per LDS.128.  Row hits are reduced within the group with
+// shuffles into per-CTA shared counters; the last CTA publishes counts and
+// the fused Eq. 1 fitness.
 // ---------------------------------------------------------------------------
-template <int RPG, int RPL, int NCW, bool kEpsZero>
+template <class Walker, int NCW>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     count_tma_kernel(const __grid_constant__ CUtensorMap tmap, const CountParams p) {
+    constexpr int RPG = Walker::kRowsPerTile;
+    constexpr int RPL = Walker::kRowsPerLane;
     constexpr int GL = RPG / RPL;    // lanes per group
     constexpr int GW = 32 / GL;      // groups per warp
     static_assert(GL >= 1 && GL <= 32 && (32 % GL) == 0, "bad lane grouping");
-    constexpr int kColBytesShift = (RPG == 32) ? 8 : (RPG == 16) ? 7 : (RPG == 8) ? 6 : (RPG == 4) ? 5 : 4;
-    static_assert((1 << kColBytesShift) == RPG * 8, "RPG must be a power of two in [2,32]");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     // TMA destinations need 128-byte alignment; static shared memory (the
-    // epilogue flag) may precede the dynamic window, so align explicitly.
-    unsigned char* smem = reinterpret_cast<unsigned char*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    // epilogue flag) may precede the dynamic window, so align by offset
+    // (pointer arithmetic on the shared array keeps LDS addressing).
+    unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const uint32_t P = p.n_series;
     unsigned char* stage_base = smem;
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * p.stage_bytes);
     uint64_t* empty_bar = full_bar + kMaxStages;
-    uint32_t* s_start = reinterpret_cast<uint32_t*>(empty_bar + kMaxStages);
-    uint32_t* s_len = s_start + P;
-    uint32_t* s_order = s_len + P;
-    uint32_t* s_cnt = s_order + P;
-    uint16_t* s_cols = reinterpret_cast<uint16_t*>(s_cnt + P);
-    uint32_t* s_hist = reinterpret_cast<uint32_t*>(
-        reinterpret_cast<uintptr_t>(s_cols + p.total_len + 7) & ~uintptr_t(15));
+    const WorkList wl = carve_work_list(reinterpret_cast<unsigned char*>(empty_bar + kMaxStages), P,
+                                        p.total_len);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -291,92 +625,53 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     if (warp == NCW) {
         // ---------------- producer warp: TMA ring ----------------
         if (lane == 0) {
-            uint32_t it = 0;
-            for (uint32_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
-                const uint32_t st = it % p.stages;
-                const uint32_t round = it / p.stages;
-                mbar_wait(&empty_bar[st], (round & 1u) ^ 1u);
+            uint32_t st = 0, phase = 0;
+            for (uint32_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+                mbar_wait(&empty_bar[st], phase ^ 1u);
                 mbar_arrive_expect_tx(&full_bar[st], p.stage_bytes);
                 unsigned char* dst = stage_base + size_t(st) * p.stage_bytes;
                 for (uint32_t b = 0; b < p.n_boxes; ++b)
-                    tma_load_2d(dst + size_t(b) * p.box_cols * RPG * 8, &tmap, &full_bar[st],
-                                static_cast<int>(tile * RPG), static_cast<int>(b * p.box_cols));
+                    tma_load_2d(dst + size_t(b) * p.box_cols * Walker::kColBytes, &tmap,
+                                &full_bar[st], static_cast<int>(tile * Walker::kDim0PerTile),
+                                static_cast<int>(b * p.box_cols));
+                if (++st == p.stages) st = 0, phase ^= 1u;
             }
         }
     } else {
         // ---------------- consumer warps ----------------
-        build_work_list(p, s_start, s_len, s_order, s_cnt, s_cols, s_hist, threadIdx.x, NCW * 32, 1);
+        build_work_list(p, wl, threadIdx.x, NCW * 32, 1);
 
-        const int grp = lane / GL;               // group within warp
-        const int gl = lane % GL;                // lane within group
-        const uint32_t gmask = (GL == 32) ? 0xffffffffu : (((1u << GL) - 1u) << (grp * GL));
+        const int grp = lane / GL;   // group within warp
+        const int gl = lane % GL;    // lane within group
         const uint32_t per_round = NCW * GW;
         const uint32_t n_rounds = (P + per_round - 1) / per_round;
         const double eps = p.eps;
 
-        uint32_t it = 0;
-        for (uint32_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x, ++it) {
-            const uint32_t st = it % p.stages;
-            mbar_wait(&full_bar[st], (it / p.stages) & 1u);
-            const unsigned char* base = stage_base + size_t(st) * p.stage_bytes + gl * (RPL * 8);
+        uint32_t st = 0, phase = 0;
+        for (uint32_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+            mbar_wait(&full_bar[st], phase);
+            const unsigned char* base = stage_base + size_t(st) * p.stage_bytes + gl * Walker::kLaneBytes;
             // rows of this tile that exist (the last tile may be partial)
-            const uint32_t row0 = tile * RPG + gl * RPL;
-            const bool v0 = row0 < p.n_rows;
-            const bool v1 = (RPL == 2) && (row0 + 1 < p.n_rows);
+            const typename Walker::Mask vmask = Walker::valid(tile * RPG + gl * RPL, p.n_rows);
 
             for (uint32_t r = 0; r < n_rounds; ++r) {
                 const uint32_t g = (r * NCW + warp) * GW + grp;
-                bool ok0 = false, ok1 = false;
-                uint32_t s = 0;
-                if (g < P) {
-                    s = s_order[g];
-                    const uint32_t a = s_start[s];
-                    const uint32_t len = s_len[s];
-                    if (len <= 1) {
-                        // No adjacent pair: the reference's loop body never runs and
-                        // the row matches (fitness.hpp:80-90).
-                        ok0 = v0;
-                        ok1 = v1;
-                    } else if (RPL == 1) {
-                        double prev = *reinterpret_cast<const double*>(
-                            base + (uint32_t(s_cols[a]) << kColBytesShift));
-                        bool ok = true;
-                        for (uint32_t i = 1; i < len; ++i) {
-                            const double cur = *reinterpret_cast<const double*>(
-                                base + (uint32_t(s_cols[a + i]) << kColBytesShift));
-                            ok &= step_ok<kEpsZero>(prev, cur, eps);
-                            prev = cur;
-                        }
-                        ok0 = ok && v0;
-                    } else {
-                        double2 prev = *reinterpret_cast<const double2*>(
-                            base + (uint32_t(s_cols[a]) << kColBytesShift));
-                        bool oka = true, okb = true;
-                        for (uint32_t i = 1; i < len; ++i) {
-                            const double2 cur = *reinterpret_cast<const double2*>(
-                                base + (uint32_t(s_cols[a + i]) << kColBytesShift));
-                            oka &= step_ok<kEpsZero>(prev.x, cur.x, eps);
-                            okb &= step_ok<kEpsZero>(prev.y, cur.y, eps);
-                            prev = cur;
-                        }
-                        ok0 = oka && v0;
-                        ok1 = okb && v1;
-                    }
-                }
-                const uint32_t b0 = __ballot_sync(0xffffffffu, ok0);
-                uint32_t c = __popc(b0 & gmask);
-                if (RPL == 2) {
-                    const uint32_t b1 = __ballot_sync(0xffffffffu, ok1);
-                    c += __popc(b1 & gmask);
-                }
-                if (gl == 0 && g < P && c) s_cnt[s] += c;
+                const bool active = g < P;
+                const uint32_t len = active ? wl.slen[g] : 0u;
+                const uint32_t sst = active ? wl.sstart[g] : 0u;
+                const bool uniform = __reduce_min_sync(0xffffffffu, len) == __reduce_max_sync(0xffffffffu, len);
+                uint32_t c = active ? Walker::count(base, wl.pcols + sst, len, uniform, eps, vmask) : 0u;
+#pragma unroll
+                for (int o = GL / 2; o >= 1; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                if (gl == 0 && active && c) wl.cnt[g] += c;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);
+            if (++st == p.stages) st = 0, phase ^= 1u;
         }
     }
     __syncthreads();
-    count_epilogue(p, s_cnt, s_len);
+    count_epilogue(p, wl.cnt, wl.sl);
 }
 
 // ---------------------------------------------------------------------------
@@ -418,7 +713,105 @@ __global__ void __launch_bounds__(256)
         if (lane == 0 && c) atomicAdd(&s_cnt[s], c);
     }
     __syncthreads();
-    count_epilogue(p, s_cnt, s_len);
+    count_epilogue(p, s_cnt, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// K4: rank layout builder (one CTA per row, rows [0, ld) incl. padding).
+// Keys: the row's values v_j (plane 0) and, with PLANES == 2, fl(v_j + eps)
+// computed exactly as the reference does (fitness.hpp:63, `cur + epsilon`).
+// Bitonic sort in shared memory, dense ranks by a block scan of "new value"
+// flags, scatter to the interleaved layout read by RankWalker.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t sortable_key(double x) {
+    if (x != x) return ~0ull;  // NaN: not a value (fails every comparison)
+    if (x == 0.0) x = 0.0;     // -0.0 and +0.0 compare equal
+    const uint64_t u = static_cast<uint64_t>(__double_as_longlong(x));
+    return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+template <int PLANES>
+__global__ void __launch_bounds__(256)
+    rank_build_kernel(const double* __restrict__ mat, uint32_t ld, uint32_t n_rows,
+                      uint32_t n_cols, double eps, uint32_t Kp, uint16_t* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* key = reinterpret_cast<uint64_t*>(smem);
+    uint32_t* pay = reinterpret_cast<uint32_t*>(key + Kp);
+    uint32_t* rk = pay + Kp;
+    uint32_t* wsum = rk + Kp;
+    const uint32_t r = blockIdx.x;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const size_t cs = PLANES == 2 ? size_t(ld) * 2 : size_t(ld);  // u16 per column
+    auto at = [&](uint32_t c, uint32_t plane) -> size_t {
+        return PLANES == 2 ? c * cs + (r >> 2) * 8 + plane * 4 + (r & 3) : c * cs + r;
+    };
+    if (r >= n_rows) {  // padding rows: fail every test
+        for (uint32_t c = tid; c < n_cols; c += nt) {
+            if (PLANES == 2) {
+                out[at(c, 0)] = 0xffff;
+                out[at(c, 1)] = 0x8000;
+            } else {
+                out[at(c, 0)] = 0x8000;
+            }
+        }
+        return;
+    }
+    const uint32_t K = PLANES * n_cols;
+    for (uint32_t i = tid; i < Kp; i += nt) {
+        uint64_t k = ~0ull;
+        uint32_t pl = 0xffffffffu;
+        if (i < K) {
+            const uint32_t plane = i >= n_cols ? 1u : 0u;
+            const uint32_t c = i - plane * n_cols;
+            double v = mat[size_t(c) * ld + r];
+            if (plane) v = __dadd_rn(v, eps);
+            k = sortable_key(v);
+            pl = c | (plane << 16);
+        }
+        key[i] = k;
+        pay[i] = pl;
+    }
+    __syncthreads();
+    for (uint32_t size = 2; size <= Kp; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = tid; i < Kp / 2; i += nt) {
+                const uint32_t lo = 2 * i - (i & (stride - 1));
+                const uint32_t hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const uint64_t a = key[lo], b = key[hi];
+                if ((a > b) == up) {
+                    key[lo] = b;
+                    key[hi] = a;
+                    const uint32_t t = pay[lo];
+                    pay[lo] = pay[hi];
+                    pay[hi] = t;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    auto is_new = [&](uint32_t i) -> uint32_t {
+        return key[i] != ~0ull && (i == 0 || key[i] != key[i - 1]) ? 1u : 0u;
+    };
+    block_exclusive_scan(Kp, is_new, rk, wsum, tid, nt, 0);
+    __syncthreads();
+    for (uint32_t i = tid; i < Kp; i += nt) {
+        const uint32_t pl = pay[i];
+        if (pl == 0xffffffffu) continue;
+        const uint32_t c = pl & 0xffffu, plane = pl >> 16;
+        uint16_t v;
+        if (key[i] == ~0ull) v = plane ? 0x8000 : 0xffff;  // NaN
+        else v = static_cast<uint16_t>((rk[i] + is_new(i)) | 0x8000u);
+        out[at(c, plane)] = v;
+    }
+}
+
+// Sets *flag if any real (non-padding) cell of the column-major matrix is NaN.
+__global__ void has_nan_kernel(const double* __restrict__ mat, size_t ld, size_t n_rows, size_t n,
+                               int* __restrict__ flag) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+        if ((i % ld) < n_rows && mat[i] != mat[i]) *flag = 1;
 }
 
 // ---------------------------------------------------------------------------

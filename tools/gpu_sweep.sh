@@ -1,0 +1,16 @@
+# Kernel-configuration sweep on the C4 workload (bench.py, no CPU baseline).
+# usage: bash tools/gpu_sweep.sh "<env1>" "<env2>" ...   (each "K=V K2=V2")
+mkdir -p gpurun_out
+out=gpurun_out/sweep.log
+: > $out
+for cfg in "$@"; do
+  echo "== $cfg" >> $out
+  env $cfg timeout 300 python bench.py --steps 400 --warmup 5 --no-cpu-baseline ${BENCH_ARGS:-} 2>&1 | \
+    python -c "import sys,json
+for l in sys.stdin:
+    l=l.strip()
+    if l.startswith('{'):
+        d=json.loads(l); r=d['roofline'] or {}
+        print('value %.3e  us/launch %s  frac %s  e2e %s  cfg %s' % (d['value'], r.get('avg_launch_us'), r.get('frac'), (d['e2e'] or {}).get('value'), d['kernel_config']))
+    else: print(l[:300])" >> $out
+done
