@@ -143,6 +143,13 @@ int ebic_count_matches_device(ebic_ctx* ctx, const uint64_t* d_offsets, const ui
 int ebic_fitness_device(ebic_ctx* ctx, const uint64_t* d_counts, const uint64_t* d_offsets,
                         size_t n_series, uint64_t sigma, double* d_fitness_out, void* stream);
 
+/* Diagnostics: per-CTA %globaltimer stamps (ns) of the last count launch on
+ * shard 0 -- [start, work list built, tiles done, epilogue done, partial
+ * counts flushed, arrival counted, -, -] per CTA -- recorded only when the
+ * context was created with EBIC_PHASE_TIMING=1 in the environment.  Copies
+ * min(grid, max_ctas) x 8 values; *n_ctas = grid. */
+int ebic_ctx_phase_times(ebic_ctx* ctx, uint64_t* stamps_out, size_t max_ctas, size_t* n_ctas);
+
 /* ---- row membership (Steps 6-7) ----------------------------------------- */
 
 /* Per-series row bitmasks over the context's rows (words = ceil(n_rows/64),

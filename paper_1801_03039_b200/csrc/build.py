@@ -1,6 +1,7 @@
 """In-tree build of the product library ``libebic_b200.so`` (sm_100a only).
 
-Invoked by ``__graft_entry__.build()`` and ``python -m paper_1801_03039_b200._build``.
+Invoked by ``__graft_entry__.build()`` and ``python paper_1801_03039_b200/csrc/build.py``
+(a standalone script: importing the package itself would load the library it builds).
 nvcc cross-compiles for sm_100a without a GPU.  The library statically links the
 CUDA runtime so the .so that travels with gpurun is self-contained.
 """
@@ -11,9 +12,9 @@ import subprocess
 import sys
 from pathlib import Path
 
-PKG = Path(__file__).resolve().parent
+CSRC = Path(__file__).resolve().parent
+PKG = CSRC.parent
 REPO = PKG.parent
-CSRC = PKG / "csrc"
 LIB = PKG / "libebic_b200.so"
 SOURCES = [CSRC / "ebic_b200.cu", CSRC / "synth.cpp"]
 DEPS = SOURCES + [CSRC / "kernels.cuh", REPO / "include" / "ebic_b200.h"]

@@ -105,6 +105,7 @@ struct CountConfig {
     int rpg = 0;        // rows per tile (0 = direct kernel)
     int rpl = 1;        // rows per lane
     int ncw = 16;       // consumer warps per CTA
+    int slice = 0;      // rank layout: bytes per staged column slice (64 or 128)
     int stages = 0;
     uint32_t box_cols = 0, n_boxes = 0, stage_bytes = 0;
 };
@@ -124,6 +125,7 @@ struct RankLayout {
     uint16_t* d = nullptr;
     CUtensorMap tmap;
     bool tmap_ok = false;
+    int tmap_slice = 0;
     uint64_t last_use = 0;
 };
 
@@ -142,14 +144,15 @@ struct Shard {
     // scratch
     unsigned char* d_in = nullptr;
     size_t d_in_cap = 0;
-    unsigned long long* d_acc = nullptr;
-    size_t acc_cap = 0;
+    uint32_t* d_partial = nullptr;   // count-kernel reduction scratch
+    size_t partial_cap = 0;          // u32 elements
     unsigned int* d_done = nullptr;
     unsigned char* d_out = nullptr;
     size_t d_out_cap = 0;
     unsigned char* h_pin = nullptr;
     size_t h_pin_cap = 0;
     Tables tables;
+    unsigned long long* d_phase = nullptr;  // EBIC_PHASE_TIMING: per-CTA phase stamps
     RankLayout ranks[2];
     uint64_t rank_clock = 0;
     int has_nan = -1;  // -1 unknown
@@ -177,14 +180,16 @@ void grow_pinned(unsigned char** p, size_t* cap, size_t need) {
     *cap = n;
 }
 
-void ensure_acc(Shard& s, size_t P) {
-    if (P <= s.acc_cap) return;
-    if (s.d_acc) CK(cudaFree(s.d_acc));
-    s.d_acc = nullptr;
-    const size_t n = std::max(P, s.acc_cap * 2);
-    CK(cudaMalloc(&s.d_acc, n * sizeof(unsigned long long)));
-    CK(cudaMemsetAsync(s.d_acc, 0, n * sizeof(unsigned long long), s.stream));
-    s.acc_cap = n;
+// Reduction scratch of one count launch: (grid + groups) rows of P counters.
+void ensure_partial(Shard& s, size_t P, int grid) {
+    const size_t gsz = reduce_group_size((uint32_t)grid);
+    const size_t need = (size_t(grid) + (grid + gsz - 1) / gsz) * P;
+    if (need <= s.partial_cap) return;
+    if (s.d_partial) CK(cudaFree(s.d_partial));
+    s.d_partial = nullptr;
+    const size_t n = std::max(need, s.partial_cap * 2);
+    CK(cudaMalloc(&s.d_partial, n * sizeof(uint32_t)));
+    s.partial_cap = n;
 }
 
 }  // namespace
@@ -211,8 +216,12 @@ void upload_shard(Shard& s, const double* src_rows, size_t n_cols, bool src_on_d
     CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     s.ld = std::max<size_t>(64, (s.rows + 63) / 64 * 64);
     CK(cudaMalloc(&s.d_mat, s.ld * n_cols * sizeof(double)));
-    CK(cudaMalloc(&s.d_done, sizeof(unsigned int)));
-    CK(cudaMemsetAsync(s.d_done, 0, sizeof(unsigned int), s.stream));
+    CK(cudaMalloc(&s.d_done, (kMaxGroups + 1) * sizeof(unsigned int)));
+    if (env_int("EBIC_PHASE_TIMING", 0)) {
+        CK(cudaMalloc(&s.d_phase, 4096 * 8 * sizeof(unsigned long long)));
+        CK(cudaMemsetAsync(s.d_phase, 0, 4096 * 8 * sizeof(unsigned long long), s.stream));
+    }
+    CK(cudaMemsetAsync(s.d_done, 0, (kMaxGroups + 1) * sizeof(unsigned int), s.stream));
 
     // Stage <= 64 MB of rows at a time (and < 2^21 rows: grid.y limit).
     size_t chunk = std::max<size_t>(32, (64ull << 20) / (n_cols * sizeof(double)));
@@ -309,13 +318,18 @@ CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int
     const int want_ncw = env_int("EBIC_NCW", 0);
     const size_t budget = (size_t)s.max_smem;
     if (rank_planes) {
+        const int want_slice = env_int("EBIC_SLICE", 0);
         for (int min_stages : {3, 2}) {
-            CountConfig c;
-            c.layout = rank_planes;
-            c.rpg = rank_planes == 2 ? 32 : 64;
-            c.rpl = rank_planes == 2 ? 4 : 8;
-            c.ncw = want_ncw == 16 ? 16 : 32;
-            if (fit_ring(c, n_cols, 128, P, L, budget, min_stages, want_stages)) return c;
+            for (int slice : {128, 64}) {
+                if (want_slice && slice != want_slice) continue;
+                CountConfig c;
+                c.layout = rank_planes;
+                c.slice = slice;
+                c.rpg = slice / (2 * rank_planes);
+                c.rpl = rank_planes == 2 ? 4 : 8;
+                c.ncw = want_ncw == 16 ? 16 : 32;
+                if (fit_ring(c, n_cols, slice, P, L, budget, min_stages, want_stages)) return c;
+            }
         }
     }
     for (int min_stages : {3, 2}) {
@@ -359,13 +373,23 @@ void launch_f64(bool e0, const CUtensorMap& tm, const CountParams& p, int grid, 
 void launch_tma(const CountConfig& c, bool e0, const CUtensorMap& tm, const CountParams& p,
                 int grid, size_t smem, cudaStream_t st) {
     if (c.layout) {
-        const bool n16 = c.ncw == 16;
+        const bool n16 = c.ncw == 16, s64 = c.slice == 64;
         if (c.layout == 2) {
-            if (n16) launch_tma_t<RankWalker<2>, 16>(tm, p, grid, smem, st);
-            else launch_tma_t<RankWalker<2>, 31>(tm, p, grid, smem, st);
+            if (s64) {
+                if (n16) launch_tma_t<RankWalker<2, 64>, 16>(tm, p, grid, smem, st);
+                else launch_tma_t<RankWalker<2, 64>, 31>(tm, p, grid, smem, st);
+            } else {
+                if (n16) launch_tma_t<RankWalker<2, 128>, 16>(tm, p, grid, smem, st);
+                else launch_tma_t<RankWalker<2, 128>, 31>(tm, p, grid, smem, st);
+            }
         } else {
-            if (n16) launch_tma_t<RankWalker<1>, 16>(tm, p, grid, smem, st);
-            else launch_tma_t<RankWalker<1>, 31>(tm, p, grid, smem, st);
+            if (s64) {
+                if (n16) launch_tma_t<RankWalker<1, 64>, 16>(tm, p, grid, smem, st);
+                else launch_tma_t<RankWalker<1, 64>, 31>(tm, p, grid, smem, st);
+            } else {
+                if (n16) launch_tma_t<RankWalker<1, 128>, 16>(tm, p, grid, smem, st);
+                else launch_tma_t<RankWalker<1, 128>, 31>(tm, p, grid, smem, st);
+            }
         }
         CK(cudaGetLastError());
         return;
@@ -448,10 +472,11 @@ RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
 }
 
 const CUtensorMap& rank_tensor_map(RankLayout& rl, const Shard& s, size_t n_cols, const CountConfig& cfg) {
-    if (!rl.tmap_ok) {
+    if (!rl.tmap_ok || rl.tmap_slice != cfg.slice) {
+        rl.tmap_slice = cfg.slice;
         cuuint64_t dims[2] = {(cuuint64_t)(s.ld * rl.planes), (cuuint64_t)n_cols};
         cuuint64_t strides[1] = {(cuuint64_t)(s.ld * rl.planes * sizeof(uint16_t))};
-        cuuint32_t box[2] = {64u, cfg.box_cols};  // 128 bytes per column slice
+        cuuint32_t box[2] = {(cuuint32_t)(cfg.slice / 2), cfg.box_cols};  // one column slice
         cuuint32_t estr[2] = {1, 1};
         CUresult r = tensor_map_encoder()(&rl.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, rl.d, dims,
                                           strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -492,11 +517,10 @@ const Tables& ensure_tables(Shard& s, uint64_t sigma, size_t total_rows) {
 // Launches the count kernel for one shard.  All pointers are device pointers.
 void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t* d_cols, size_t P,
                   size_t L, double eps, uint64_t* d_counts, double* d_fit, uint64_t sigma,
-                  cudaStream_t st) {
+                  cudaStream_t st, uint64_t cols_base) {
     if (P == 0) return;
     if (P > 0xffffffffull || L > 0xffffffffull || s.rows > 0xffffffffull)
         fail(EBIC_ERR_INVALID_ARGUMENT, "population or shard too large for one launch");
-    ensure_acc(s, P);
     CountParams p{};
     p.offsets = d_off;
     p.cols = d_cols;
@@ -506,12 +530,15 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
     p.n_cols = (uint32_t)ctx.n_cols;
     p.eps = eps;
     p.sigma = sigma;
-    p.acc = s.d_acc;
     p.done = s.d_done;
     p.counts_out = d_counts;
     p.fitness_out = d_fit;
     p.matrix = s.d_mat;
     p.ld = (uint32_t)s.ld;
+    p.cols_base = cols_base;
+    p.sched_static = (uint32_t)env_int("EBIC_SCHED_STATIC", 0);
+    p.max_parts = (uint32_t)env_int("EBIC_MAX_PARTS", 8);
+    p.phase_ns = s.d_phase;
     if (d_fit) {
         const Tables& t = ensure_tables(s, sigma, ctx.total_rows);
         p.logt = t.d_log;
@@ -532,6 +559,8 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         if (g_env > 0) grid = std::min<int>(g_env, (int)p.n_tiles);
         s.last_grid = grid;
         s.last_cfg = c;
+        ensure_partial(s, P, grid);
+        p.partial = s.d_partial;
         const CUtensorMap& tm = c.layout ? rank_tensor_map(*rl, s, ctx.n_cols, c) : tensor_map(s, ctx.n_cols, c);
         launch_tma(c, e0, tm, p, grid, smem, st);
     } else {
@@ -540,6 +569,8 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         const int grid = (int)((s.rows + 255) / 256);
         s.last_grid = grid;
         s.last_cfg = c;
+        ensure_partial(s, P, grid);
+        p.partial = s.d_partial;
         if (e0) {
             CK(cudaFuncSetAttribute(count_direct_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             count_direct_kernel<true><<<grid, 256, smem, st>>>(p);
@@ -582,7 +613,7 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
     for (Shard& s : ctx.shards) {
         DeviceGuard g(s.device);
         grow_pinned(&s.h_pin, &s.h_pin_cap, in_bytes + out_bytes + 16);
-        grow_device(&s.d_in, &s.d_in_cap, in_bytes);
+        grow_device(&s.d_in, &s.d_in_cap, in_bytes + 64);
         grow_device(&s.d_out, &s.d_out_cap, out_bytes);
         static_assert(sizeof(size_t) == sizeof(uint64_t), "size_t must be 64-bit");
         std::memcpy(s.h_pin, off, off_bytes);
@@ -600,7 +631,7 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
             while (s1 < P && s1 - s0 < kMaxSeriesPerLaunch && off[s1 + 1] - off[s0] <= kMaxLenPerLaunch) ++s1;
             if (s1 == s0) s1 = s0 + 1;  // a single over-long series still gets its own launch
             launch_count(ctx, s, d_off + s0, d_cols, s1 - s0, off[s1] - off[s0], eps, d_counts + s0,
-                         d_fit ? d_fit + s0 : nullptr, sigma, s.stream);
+                         d_fit ? d_fit + s0 : nullptr, sigma, s.stream, off[s0]);
             s0 = s1;
         }
         CK(cudaMemcpyAsync(s.h_pin + in_bytes, s.d_out, d_fit ? out_bytes : P * 8,
@@ -683,13 +714,14 @@ void free_shard(Shard& s) {
     if (s.stream) cudaStreamSynchronize(s.stream);
     cudaFree(s.d_mat);
     cudaFree(s.d_in);
-    cudaFree(s.d_acc);
+    cudaFree(s.d_partial);
     cudaFree(s.d_done);
     cudaFree(s.d_out);
     if (s.h_pin) cudaFreeHost(s.h_pin);
     cudaFree(s.tables.d_log);
     cudaFree(s.tables.d_exp);
     for (RankLayout& rl : s.ranks) cudaFree(rl.d);
+    cudaFree(s.d_phase);
     if (s.stream) cudaStreamDestroy(s.stream);
 }
 
@@ -874,7 +906,7 @@ int ebic_count_matches_device(ebic_ctx* ctx, const uint64_t* d_offsets, const ui
             fail(EBIC_ERR_INVALID_ARGUMENT, "device batch exceeds 4096 series / 16384 columns; split it");
         cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream
         launch_count(*ctx, s, d_offsets, d_cols, n_series, total_len, eps, d_counts_out, d_fitness_out,
-                     sigma, st);
+                     sigma, st, 0);  // device CBF: offsets[0] == 0 (cbf.hpp:43-52)
     });
 }
 
@@ -889,6 +921,19 @@ int ebic_fitness_device(ebic_ctx* ctx, const uint64_t* d_counts, const uint64_t*
         fitness_kernel<<<(unsigned)((n_series + 255) / 256), 256, 0, st>>>(
             d_counts, d_offsets, (uint32_t)n_series, sigma, t.d_log, t.d_exp, d_fitness_out);
         CK(cudaGetLastError());
+    });
+}
+
+int ebic_ctx_phase_times(ebic_ctx* ctx, uint64_t* stamps_out, size_t max_ctas, size_t* n_ctas) {
+    return guarded([&] {
+        Shard& s = single_shard(ctx);
+        DeviceGuard g(s.device);
+        if (!n_ctas) fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+        *n_ctas = s.d_phase ? (size_t)s.last_grid : 0;
+        if (!s.d_phase || !stamps_out) return;
+        const size_t n = std::min<size_t>(max_ctas, (size_t)s.last_grid);
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(stamps_out, s.d_phase, n * 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     });
 }
 

@@ -19,6 +19,17 @@
 namespace ebic_b200 {
 
 constexpr int kMaxStages = 8;
+// Grid reduction tree of the count kernels: CTAs publish per-series partial
+// counts into their own row; the last CTA of each group of kGroupMin+ CTAs
+// sums its group; the last group reducer finalises.  No atomics on data (a
+// 148-way atomic reduction into the same P addresses serialises in the L2
+// atomic units), two atomic tickets per CTA at most.
+constexpr int kMaxGroups = 64;
+constexpr int kGroupMin = 16;
+__host__ __device__ inline uint32_t reduce_group_size(uint32_t grid) {
+    const uint32_t g = (grid + kMaxGroups - 1) / kMaxGroups;
+    return g < kGroupMin ? kGroupMin : g;
+}
 constexpr int kLenBuckets = 64;  // length histogram buckets for the work sort
 
 // ---------------------------------------------------------------------------
@@ -137,15 +148,25 @@ struct CountParams {
     uint32_t stages;
     double eps;
     uint64_t sigma;
-    unsigned long long* __restrict__ acc;  // [P] zero on entry; zero again on exit
-    unsigned int* __restrict__ done;       // grid arrival counter (zero on entry and exit)
+    uint32_t* __restrict__ partial;        // [(grid + groups) * P] reduction scratch
+    unsigned int* __restrict__ done;       // [kMaxGroups + 1] tickets (zero on entry and exit)
     uint64_t* __restrict__ counts_out;     // [P]
     double* __restrict__ fitness_out;      // [P] or nullptr
     const double* __restrict__ logt;       // fitness tables (nullptr if no fitness)
     const double* __restrict__ expt;
     const double* __restrict__ matrix;     // column-major (direct kernel only)
     uint32_t ld;                           // leading dimension (direct kernel only)
+    uint64_t cols_base;                    // == offsets[0] (host-known; no dependent load)
+    uint32_t sched_static;                 // debug: static chunk assignment
+    uint32_t max_parts;                    // tail split of the last wave (1 = off)
+    unsigned long long* __restrict__ phase_ns;  // optional [grid][8] %globaltimer stamps
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Shared-memory work list of one count launch (P series, L column entries):
 //   s_sl     u32[P]   slot -> series id (slots are length-sorted)
@@ -157,12 +178,20 @@ struct CountParams {
 //                     (16-byte aligned: one LDS.128 fetches 8 column indices)
 //   s_raw    u16[L]   the launch's column indices (prologue scratch)
 //   s_hist   u32[kLenBuckets], s_wsum u32[32]
+// The column-list area doubles as scratch for the stable scatter's per-block
+// bucket counts ([ceil(P/32)][kLenBuckets] u32), so it is at least that big.
+__host__ __device__ inline size_t pcols_area_bytes(uint32_t P, uint32_t L) {
+    const size_t cols = 2ull * (L + 7ull * P) + 16;
+    const size_t scratch = 4ull * kLenBuckets * ((P + 31) / 32);
+    return cols > scratch ? cols : scratch;
+}
+
 __host__ __device__ inline size_t count_meta_bytes(uint32_t P, uint32_t total_len) {
     size_t b = 16ull * P + 4ull * (P + 1);
     b = (b + 15) & ~size_t(15);
-    b += 2ull * (total_len + 7ull * P) + 16;
+    b += pcols_area_bytes(P, total_len);
     b = (b + 15) & ~size_t(15);
-    b += 2ull * total_len + 16;
+    b += 2ull * total_len + 32;
     b = (b + 15) & ~size_t(15);
     return b + 4ull * kLenBuckets + 4ull * 32 + 16;
 }
@@ -195,9 +224,9 @@ __device__ __forceinline__ WorkList carve_work_list(unsigned char* p, uint32_t P
     size_t off = 16ull * P + 4ull * (P + 1);
     unsigned char* q = align16(p, off);
     w.pcols = reinterpret_cast<uint16_t*>(q);
-    q = align16(q, 2ull * (L + 7ull * P) + 16);
+    q = align16(q, pcols_area_bytes(P, L));
     w.raw = reinterpret_cast<uint16_t*>(q);
-    q = align16(q, 2ull * L + 16);
+    q = align16(q, 2ull * L + 32);
     w.hist = reinterpret_cast<uint32_t*>(q);
     w.wsum = w.hist + kLenBuckets;
     return w;
@@ -248,11 +277,33 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
                                                 int nthreads, int bar_id) {
     const uint32_t P = p.n_series, L = p.total_len;
     // A launch may cover a slice of a larger population: column positions are
-    // taken relative to offsets[0].
-    const uint64_t base = p.offsets[0];
-    for (uint32_t s = tid; s <= P; s += nthreads) w.rel[s] = static_cast<uint32_t>(p.offsets[s] - base);
-    const uint16_t* gcols = p.cols + base;
-    for (uint32_t i = tid; i < L; i += nthreads) w.raw[i] = gcols[i];
+    // taken relative to offsets[0] (== cols_base, passed by value so the loads
+    // below do not wait on it).  The column indices are fetched as whole
+    // 16-byte words from the aligned word containing cols[base]; `shift`
+    // re-bases positions inside w.raw.  Both streams are issued before any
+    // shared-memory store so they share one round trip.
+    const uint64_t base = p.cols_base;
+    const uint16_t* src = p.cols + base;
+    const uint32_t shift = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) & 15u) >> 1);
+    const uint4* vsrc = reinterpret_cast<const uint4*>(src - shift);
+    const uint32_t n_vec = (shift + L + 7u) >> 3;
+    constexpr int kPer = 4;  // loads in flight per thread per pass
+    for (uint32_t s0 = tid; s0 <= P || s0 < n_vec; s0 += kPer * nthreads) {
+        uint64_t o[kPer];
+        uint4 v[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const uint32_t i = s0 + k * nthreads;
+            if (i <= P) o[k] = __ldg(p.offsets + i);
+            if (i < n_vec) v[k] = __ldg(vsrc + i);
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const uint32_t i = s0 + k * nthreads;
+            if (i <= P) w.rel[i] = static_cast<uint32_t>(o[k] - base) + shift;
+            if (i < n_vec) reinterpret_cast<uint4*>(w.raw)[i] = v[k];
+        }
+    }
     for (int b = tid; b < kLenBuckets; b += nthreads) w.hist[b] = 0;
     named_bar_sync(bar_id, nthreads);
     for (uint32_t s = tid; s < P; s += nthreads) {
@@ -277,12 +328,52 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
         w.hist[tid + 32] = total_a + z - b;
     }
     named_bar_sync(bar_id, nthreads);
-    for (uint32_t s = tid; s < P; s += nthreads) {
-        const uint32_t len = w.rel[s + 1] - w.rel[s];
-        const uint32_t g = atomicAdd(&w.hist[len < kLenBuckets ? len : kLenBuckets - 1], 1u);
-        w.sl[g] = s;
-        w.slen[g] = len;
-        w.cnt[g] = 0;
+    // Deterministic (stable) scatter: within a length bucket the slots follow
+    // series order, so every CTA derives the same slot order and a chunk range
+    // names the same series on every CTA (tail-split tiles are shared between
+    // CTAs by chunk range).  Rank within the bucket = same-bucket series in
+    // earlier 32-series blocks (scanned per bucket) + in-warp rank
+    // (__match_any_sync).  The per-block counts live in the not-yet-built
+    // column-list area.
+    {
+        const uint32_t nblk = (P + 31) / 32;
+        uint32_t* wh = reinterpret_cast<uint32_t*>(w.pcols);  // [nblk][kLenBuckets]
+        const int lane = tid & 31, nw = nthreads >> 5;
+        const uint32_t lt = (1u << lane) - 1u;
+        for (uint32_t i = tid; i < nblk * kLenBuckets; i += nthreads) wh[i] = 0;
+        named_bar_sync(bar_id, nthreads);
+        auto bucket_of = [&](uint32_t s, uint32_t& len) -> uint32_t {
+            len = s < P ? w.rel[s + 1] - w.rel[s] : 0u;
+            return s < P ? (len < kLenBuckets ? len : kLenBuckets - 1) : 0xffffu;
+        };
+        for (uint32_t blk = tid >> 5; blk < nblk; blk += nw) {
+            uint32_t len;
+            const uint32_t bkt = bucket_of(blk * 32 + lane, len);
+            const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
+            if (bkt != 0xffffu && lane == __ffs(peers) - 1) wh[blk * kLenBuckets + bkt] = __popc(peers);
+        }
+        named_bar_sync(bar_id, nthreads);
+        if (tid < kLenBuckets) {
+            uint32_t run = w.hist[tid];
+            for (uint32_t blk = 0; blk < nblk; ++blk) {
+                const uint32_t t = wh[blk * kLenBuckets + tid];
+                wh[blk * kLenBuckets + tid] = run;
+                run += t;
+            }
+        }
+        named_bar_sync(bar_id, nthreads);
+        for (uint32_t blk = tid >> 5; blk < nblk; blk += nw) {
+            uint32_t len;
+            const uint32_t s = blk * 32 + lane;
+            const uint32_t bkt = bucket_of(s, len);
+            const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
+            if (bkt != 0xffffu) {
+                const uint32_t g = wh[blk * kLenBuckets + bkt] + __popc(peers & lt);
+                w.sl[g] = s;
+                w.slen[g] = len;
+                w.cnt[g] = 0;
+            }
+        }
     }
     named_bar_sync(bar_id, nthreads);
     block_exclusive_scan(P, [&](uint32_t g) { return (w.slen[g] + 7u) & ~7u; }, w.sstart, w.wsum,
@@ -297,34 +388,79 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
     named_bar_sync(bar_id, nthreads);
 }
 
-// Grid-wide reduction tail shared by the count kernels: per-CTA counts are
-// added to the global accumulator; the last CTA to arrive publishes the final
-// counts (and Eq. 1 fitness when tables are given) and re-zeroes the
-// accumulator and arrival counter for the next launch.  `slot_series` maps a
-// counter slot to its series id (nullptr = identity).
+// Ticket with release (publishes this CTA's prior writes, ordered before it
+// by the preceding __syncthreads) and acquire (makes the other CTAs' published
+// writes visible to the CTA that draws the last ticket) -- the
+// bar.sync + red/atom.release.gpu pattern of CUTLASS's grid barrier.
+__device__ __forceinline__ uint32_t ticket_acq_rel(unsigned int* ctr) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+    return old;
+}
+
+// Sum of rows[r * P + s] for r in [lo, hi): loads issued 16 at a time so the
+// L2 round trips overlap (L2-only loads: the rows were written by other SMs).
+__device__ __forceinline__ uint64_t sum_rows(const uint32_t* rows, size_t P, uint32_t s,
+                                             uint32_t lo, uint32_t hi) {
+    uint64_t c = 0;
+    for (uint32_t b = lo; b < hi; b += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = (b + k < hi) ? __ldcg(rows + size_t(b + k) * P + s) : 0u;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) c += v[k];
+    }
+    return c;
+}
+
+// Grid-wide reduction tail shared by the count kernels (see kMaxGroups): the
+// final CTA publishes counts (and Eq. 1 fitness when tables are given) and
+// every ticket counter is left at zero for the next launch.  Integer sums:
+// the result does not depend on arrival order (fitness.hpp:17-19).
+// `slot_series` maps a counter slot to its series id (nullptr = identity).
 __device__ __forceinline__ void count_epilogue(const CountParams& p, const uint32_t* s_cnt,
                                                const uint32_t* slot_series) {
-    const uint32_t P = p.n_series;
-    for (uint32_t g = threadIdx.x; g < P; g += blockDim.x) {
-        const uint32_t c = s_cnt[g];
-        const uint32_t s = slot_series ? slot_series[g] : g;
-        if (c) atomicAdd(&p.acc[s], static_cast<unsigned long long>(c));
-    }
-    __threadfence();
-    __syncthreads();
+    const uint32_t P = p.n_series, G = gridDim.x;
+    const uint32_t gsz = reduce_group_size(G);
+    const uint32_t n_groups = (G + gsz - 1) / gsz;
+    const uint32_t grp = blockIdx.x / gsz;
+    const uint32_t g_lo = grp * gsz, g_hi = min(G, g_lo + gsz);
+    uint32_t* rows = p.partial;                   // [G][P]
+    uint32_t* grows = p.partial + size_t(G) * P;  // [n_groups][P]
+    unsigned long long* stamp = p.phase_ns ? p.phase_ns + 8ull * blockIdx.x : nullptr;
     __shared__ int s_last;
-    if (threadIdx.x == 0) s_last = (atomicAdd(p.done, 1u) == gridDim.x - 1);
+
+    for (uint32_t g = threadIdx.x; g < P; g += blockDim.x)
+        rows[size_t(blockIdx.x) * P + (slot_series ? slot_series[g] : g)] = s_cnt[g];
+    __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[4] = global_ns();
+    if (threadIdx.x == 0) s_last = ticket_acq_rel(&p.done[grp]) == (g_hi - g_lo) - 1;
+    __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[5] = global_ns();
+    if (!s_last) return;
+
+    // last CTA of its group: sum the group's rows
+    for (uint32_t s = threadIdx.x; s < P; s += blockDim.x)
+        grows[size_t(grp) * P + s] = static_cast<uint32_t>(sum_rows(rows, P, s, g_lo, g_hi));
+    __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[6] = global_ns();
+    if (threadIdx.x == 0) {
+        p.done[grp] = 0u;
+        s_last = ticket_acq_rel(&p.done[kMaxGroups]) == n_groups - 1;
+    }
     __syncthreads();
     if (!s_last) return;
-    __threadfence();
+    if (stamp && threadIdx.x == 0) stamp[7] = global_ns();
+
+    // last group reducer: final counts + fused Eq. 1
     for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
-        const uint64_t c = atomicExch(&p.acc[s], 0ull);
+        const uint64_t c = sum_rows(grows, P, s, 0, n_groups);
         p.counts_out[s] = c;
         if (p.fitness_out)
             p.fitness_out[s] = fitness_from_tables(c, p.offsets[s + 1] - p.offsets[s], p.sigma,
                                                    p.logt, p.expt);
     }
-    if (threadIdx.x == 0) *p.done = 0u;
+    if (threadIdx.x == 0) p.done[kMaxGroups] = 0u;
 }
 
 // ---------------------------------------------------------------------------
@@ -419,10 +555,14 @@ struct F64Walker {
         }
     }
 
-    __device__ __forceinline__ static uint32_t count(const unsigned char* base, const uint16_t* pc,
-                                                     uint32_t len, bool uniform, double eps,
-                                                     Mask vm) {
-        return __popc(walk(base, pc, len, uniform, eps) & vm);
+    static constexpr int kSeriesPerGroup = 1;
+    __device__ __forceinline__ static uint32_t count_group(const unsigned char* base,
+                                                           const WorkList& wl, uint32_t g0,
+                                                           uint32_t P, bool uniform, uint32_t ulen,
+                                                           double eps, Mask vm) {
+        if (g0 >= P) return 0u;
+        const uint32_t len = uniform ? ulen : wl.slen[g0];
+        return __popc(walk(base, wl.pcols + wl.sstart[g0], len, uniform, eps) & vm);
     }
 
     __device__ __forceinline__ static uint32_t walk(const unsigned char* base, const uint16_t* pc,
@@ -466,15 +606,17 @@ struct F64Walker {
 //     8 rows (one LDS.128).
 // Tile: 128 bytes per column (32 rows x 2 planes, or 64 rows x 1 plane).
 // ---------------------------------------------------------------------------
-template <int PLANES>
+template <int PLANES, int SLICE>
 struct RankWalker {
+    static_assert(SLICE == 64 || SLICE == 128, "column slice of 64 or 128 bytes");
     static constexpr int kRowsPerLane = PLANES == 2 ? 4 : 8;
-    static constexpr int kRowsPerTile = PLANES == 2 ? 32 : 64;
+    static constexpr int kRowsPerTile = SLICE / (2 * PLANES);
     static constexpr int kLaneBytes = 16;
-    static constexpr int kColBytes = 128;
-    static constexpr int kShift = 7;
+    static constexpr int kColBytes = SLICE;
+    static constexpr int kShift = SLICE == 128 ? 7 : 6;
     static constexpr int kDim0PerTile = kRowsPerTile * PLANES;  // u16 elements
     static constexpr int kWords = kRowsPerLane / 2;           // ok words per lane
+    static constexpr int kSeriesPerGroup = 2;                 // two independent walks per group
     struct Mask {
         uint32_t m[kWords];
     };
@@ -492,6 +634,14 @@ struct RankWalker {
     }
     __device__ __forceinline__ static uint4 ld(const unsigned char* base, uint32_t col) {
         return *reinterpret_cast<const uint4*>(base + (col << kShift));
+    }
+    __device__ __forceinline__ static void load_cols(uint32_t* w, const uint16_t* pc, int L) {
+        const uint4 q0 = *reinterpret_cast<const uint4*>(pc);
+        w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
+        if (L > 8) {
+            const uint4 q1 = *reinterpret_cast<const uint4*>(pc + 8);
+            w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+        }
     }
     // One adjacent pair: ok[k] accumulates bit 15/31 per row.
     __device__ __forceinline__ static void step(uint32_t* ok, const uint4& prev, const uint4& cur) {
@@ -511,27 +661,28 @@ struct RankWalker {
         for (int k = 0; k < kWords; ++k) c += __popc(ok[k] & vm.m[k]);
         return c;
     }
+    // Two series of exactly L columns, walked interleaved (independent chains).
     template <int L>
-    __device__ __forceinline__ static uint32_t count_fixed(const unsigned char* base,
-                                                           const uint16_t* pc, const Mask& vm) {
-        uint32_t w[8];
-        const uint4 q0 = *reinterpret_cast<const uint4*>(pc);
-        w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-        if (L > 8) {
-            const uint4 q1 = *reinterpret_cast<const uint4*>(pc + 8);
-            w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-        }
-        uint32_t ok[kWords];
+    __device__ __forceinline__ static uint32_t count2_fixed(const unsigned char* base,
+                                                            const uint16_t* pa, const uint16_t* pb,
+                                                            const Mask& vm) {
+        uint32_t wa[8], wb[8];
+        load_cols(wa, pa, L);
+        load_cols(wb, pb, L);
+        uint32_t oka[kWords], okb[kWords];
 #pragma unroll
-        for (int k = 0; k < kWords; ++k) ok[k] = 0xffffffffu;
-        uint4 prev = ld(base, col_at(w, 0));
+        for (int k = 0; k < kWords; ++k) oka[k] = okb[k] = 0xffffffffu;
+        uint4 preva = ld(base, col_at(wa, 0)), prevb = ld(base, col_at(wb, 0));
 #pragma unroll
         for (int i = 1; i < L; ++i) {
-            const uint4 cur = ld(base, col_at(w, i));
-            step(ok, prev, cur);
-            prev = cur;
+            const uint4 cura = ld(base, col_at(wa, i));
+            const uint4 curb = ld(base, col_at(wb, i));
+            step(oka, preva, cura);
+            step(okb, prevb, curb);
+            preva = cura;
+            prevb = curb;
         }
-        return tally(ok, vm);
+        return tally(oka, vm) | (tally(okb, vm) << 16);
     }
     __device__ __forceinline__ static uint32_t count_any(const unsigned char* base,
                                                          const uint16_t* pc, uint32_t len,
@@ -549,26 +700,34 @@ struct RankWalker {
         }
         return tally(ok, vm);
     }
-    __device__ __forceinline__ static uint32_t count(const unsigned char* base, const uint16_t* pc,
-                                                     uint32_t len, bool uniform, double,
-                                                     const Mask& vm) {
+    // Counts of slots g0 and g0+1 (16-bit fields).  `uniform`: every slot of
+    // the warp's chunk exists and has length ulen.
+    __device__ __forceinline__ static uint32_t count_group(const unsigned char* base,
+                                                           const WorkList& wl, uint32_t g0,
+                                                           uint32_t P, bool uniform, uint32_t ulen,
+                                                           double, const Mask& vm) {
         if (uniform) {
-            switch (len) {
-                case 2: return count_fixed<2>(base, pc, vm);
-                case 3: return count_fixed<3>(base, pc, vm);
-                case 4: return count_fixed<4>(base, pc, vm);
-                case 5: return count_fixed<5>(base, pc, vm);
-                case 6: return count_fixed<6>(base, pc, vm);
-                case 7: return count_fixed<7>(base, pc, vm);
-                case 8: return count_fixed<8>(base, pc, vm);
-                case 9: return count_fixed<9>(base, pc, vm);
-                case 10: return count_fixed<10>(base, pc, vm);
-                case 11: return count_fixed<11>(base, pc, vm);
-                case 12: return count_fixed<12>(base, pc, vm);
+            const uint16_t* pa = wl.pcols + wl.sstart[g0];
+            const uint16_t* pb = wl.pcols + wl.sstart[g0 + 1];
+            switch (ulen) {
+                case 2: return count2_fixed<2>(base, pa, pb, vm);
+                case 3: return count2_fixed<3>(base, pa, pb, vm);
+                case 4: return count2_fixed<4>(base, pa, pb, vm);
+                case 5: return count2_fixed<5>(base, pa, pb, vm);
+                case 6: return count2_fixed<6>(base, pa, pb, vm);
+                case 7: return count2_fixed<7>(base, pa, pb, vm);
+                case 8: return count2_fixed<8>(base, pa, pb, vm);
+                case 9: return count2_fixed<9>(base, pa, pb, vm);
+                case 10: return count2_fixed<10>(base, pa, pb, vm);
+                case 11: return count2_fixed<11>(base, pa, pb, vm);
+                case 12: return count2_fixed<12>(base, pa, pb, vm);
                 default: break;
             }
         }
-        return count_any(base, pc, len, vm);
+        uint32_t c = 0;
+        if (g0 < P) c = count_any(base, wl.pcols + wl.sstart[g0], wl.slen[g0], vm);
+        if (g0 + 1 < P) c |= count_any(base, wl.pcols + wl.sstart[g0 + 1], wl.slen[g0 + 1], vm) << 16;
+        return c;
     }
 };
 
@@ -612,6 +771,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    unsigned long long* stamp = p.phase_ns ? p.phase_ns + 8ull * blockIdx.x : nullptr;
+    if (stamp && threadIdx.x == 0) stamp[0] = global_ns();
 
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < p.stages; ++s) {
@@ -622,12 +783,29 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     }
     __syncthreads();
 
+    // Work items.  Every full wave of tiles is one item per tile; the tiles of
+    // a final partial wave are split into `parts` items by chunk range, so the
+    // last wave keeps every CTA busy (each part re-loads its tile: a few MB of
+    // extra traffic instead of one idle tile-time on most SMs).
+    constexpr int SPG = Walker::kSeriesPerGroup;
+    constexpr uint32_t CHUNK = GW * SPG;  // slots per warp-iteration
+    const uint32_t n_chunks = (P + CHUNK - 1) / CHUNK;
+    const uint32_t G = gridDim.x;
+    const uint32_t full = (p.n_tiles / G) * G;
+    const uint32_t rem = p.n_tiles - full;
+    uint32_t parts = rem ? G / rem : 1u;
+    parts = max(1u, min(parts, min(p.max_parts, n_chunks)));
+    const uint32_t n_items = full + rem * parts;
+    __shared__ uint32_t s_next[kMaxStages];  // per-stage chunk dispenser
+
     if (warp == NCW) {
         // ---------------- producer warp: TMA ring ----------------
         if (lane == 0) {
             uint32_t st = 0, phase = 0;
-            for (uint32_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+            for (uint32_t item = blockIdx.x; item < n_items; item += G) {
+                const uint32_t tile = item < full ? item : full + (item - full) / parts;
                 mbar_wait(&empty_bar[st], phase ^ 1u);
+                s_next[st] = 0;  // published to the consumers by the arrive below (release)
                 mbar_arrive_expect_tx(&full_bar[st], p.stage_bytes);
                 unsigned char* dst = stage_base + size_t(st) * p.stage_bytes;
                 for (uint32_t b = 0; b < p.n_boxes; ++b)
@@ -640,30 +818,64 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     } else {
         // ---------------- consumer warps ----------------
         build_work_list(p, wl, threadIdx.x, NCW * 32, 1);
+        if (stamp && threadIdx.x == 0) stamp[1] = global_ns();
 
         const int grp = lane / GL;   // group within warp
         const int gl = lane % GL;    // lane within group
-        const uint32_t per_round = NCW * GW;
-        const uint32_t n_rounds = (P + per_round - 1) / per_round;
         const double eps = p.eps;
 
         uint32_t st = 0, phase = 0;
-        for (uint32_t tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+        for (uint32_t item = blockIdx.x; item < n_items; item += G) {
+            uint32_t tile = item, c_lo = 0, c_hi = n_chunks;
+            if (item >= full) {
+                const uint32_t j = item - full, part = j % parts;
+                tile = full + j / parts;
+                c_lo = part * n_chunks / parts;
+                c_hi = (part + 1) * n_chunks / parts;
+            }
             mbar_wait(&full_bar[st], phase);
             const unsigned char* base = stage_base + size_t(st) * p.stage_bytes + gl * Walker::kLaneBytes;
             // rows of this tile that exist (the last tile may be partial)
             const typename Walker::Mask vmask = Walker::valid(tile * RPG + gl * RPL, p.n_rows);
 
-            for (uint32_t r = 0; r < n_rounds; ++r) {
-                const uint32_t g = (r * NCW + warp) * GW + grp;
-                const bool active = g < P;
-                const uint32_t len = active ? wl.slen[g] : 0u;
-                const uint32_t sst = active ? wl.sstart[g] : 0u;
-                const bool uniform = __reduce_min_sync(0xffffffffu, len) == __reduce_max_sync(0xffffffffu, len);
-                uint32_t c = active ? Walker::count(base, wl.pcols + sst, len, uniform, eps, vmask) : 0u;
+            // Chunks are handed out dynamically (longest first: slots are
+            // sorted by ascending length) so the warps of the CTA finish a
+            // tile together; the next index is fetched before the current
+            // chunk is walked.
+            const uint32_t n_here = c_hi - c_lo;
+            uint32_t stat_k = warp;
+            auto grab = [&]() {
+                if (p.sched_static) {
+                    const uint32_t v = stat_k;
+                    stat_k += NCW;
+                    return v;
+                }
+                uint32_t v = 0;
+                if (lane == 0) v = atomicAdd(&s_next[st], 1u);
+                return __shfl_sync(0xffffffffu, v, 0);
+            };
+            uint32_t k = grab();
+            while (k < n_here) {
+                const uint32_t ch = c_hi - 1 - k;
+                k = grab();
+                const uint32_t first = ch * CHUNK;
+                // Slots are sorted by length, so a full chunk is uniform iff its
+                // first and last slots agree (lengths > 12 never take the
+                // unrolled path, so the unsorted overflow bucket is harmless).
+                const uint32_t ulen = wl.slen[first];
+                const bool uniform = first + CHUNK <= P && wl.slen[first + CHUNK - 1] == ulen;
+                const uint32_t g0 = first + grp * SPG;
+                uint32_t c = Walker::count_group(base, wl, g0, P, uniform, ulen, eps, vmask);
 #pragma unroll
                 for (int o = GL / 2; o >= 1; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-                if (gl == 0 && active && c) wl.cnt[g] += c;
+                if (gl == 0) {
+#pragma unroll
+                    for (int q = 0; q < SPG; ++q) {
+                        const uint32_t cq = (c >> (16 * q)) & 0xffffu;
+                        // warps on different tiles may hold the same chunk
+                        if (g0 + q < P && cq) atomicAdd(&wl.cnt[g0 + q], cq);
+                    }
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);
@@ -671,7 +883,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         }
     }
     __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[2] = global_ns();
     count_epilogue(p, wl.cnt, wl.sl);
+    if (stamp && threadIdx.x == 0) stamp[3] = global_ns();
 }
 
 // ---------------------------------------------------------------------------
