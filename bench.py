@@ -114,12 +114,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def algorithmic_bytes(rows: int, off: np.ndarray, cols: np.ndarray) -> int:
-    """rows x U x 8 (fp64 cells of the distinct columns the
-    launch references) + CBF in + counts/fitness out."""
+# bytes per matrix cell of the layout the count kernel streams (ebic_ctx_info.layout)
+LAYOUT_CELL_BYTES = {0: 8, 1: 2, 2: 4}
+LAYOUT_NAMES = {0: "fp64", 1: "rank16x1", 2: "rank16x2"}
+
+
+def algorithmic_bytes(rows: int, off: np.ndarray, cols: np.ndarray, cell_bytes: int) -> int:
+    """rows x U x b_elem (cells of the U distinct columns the
+    launch references, at the element width of the layout actually streamed:
+    8 for fp64, 4 for the two-plane exact rank layout, 2 for one plane)
+    + CBF in + counts/fitness out."""
     P = len(off) - 1
     U = len(np.unique(cols))
-    return rows * U * 8 + (P + 1) * 8 + len(cols) * 2 + P * 8 * 2
+    return rows * U * cell_bytes + (P + 1) * 8 + len(cols) * 2 + P * 8 * 2
 
 
 # ---------------------------------------------------------------------------
@@ -239,7 +246,7 @@ def run_ours(args):
             cols=torch.from_numpy(cols.view(np.int16)).to(dev),
             counts=torch.zeros(len(off) - 1, dtype=torch.int64, device=dev),
             fit=torch.zeros(len(off) - 1, dtype=torch.float64, device=dev),
-            bytes=algorithmic_bytes(hi - lo, off, cols), want=(counts, fit)))
+            want=(counts, fit)))
     # L2 eviction between timed steps by READING 512 MB (4x L2): leaves L2 full
     # of clean lines, so the timed kernel does not pay for write-backs that a
     # write-based flush would leave behind.
@@ -269,6 +276,10 @@ def run_ours(args):
     for k in range(max(args.warmup, len(dev_batches))):
         step(dev_batches[k % len(dev_batches)])
     torch.cuda.synchronize()
+    layout = ev.info().layout
+    for b, (off, cols, _, _) in zip(dev_batches, t.batches):
+        b["bytes"] = algorithmic_bytes(hi - lo, off, cols, LAYOUT_CELL_BYTES[layout])
+        b["bytes_f64"] = algorithmic_bytes(hi - lo, off, cols, 8)
     for b in dev_batches:
         step(b)
         torch.cuda.synchronize()
@@ -288,6 +299,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     series = 0
     nbytes = 0
+    nbytes_f64 = 0
     for k in range(args.steps):
         b = dev_batches[k % len(dev_batches)]
         evict_l2()                          # evict L2 (outside the events)
@@ -297,6 +309,7 @@ def run_ours(args):
         ends[k].record(stream)
         series += b["P"]
         nbytes += b["bytes"]
+        nbytes_f64 += b["bytes_f64"]
     torch.cuda.synchronize()
     if sharded:
         dist.barrier()
@@ -388,7 +401,10 @@ def run_ours(args):
                 traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
             roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": traffic,
-                    "algorithmic_bytes_per_launch": avg_bytes, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": avg_bytes,
+                    "layout": LAYOUT_NAMES[layout], "cell_bytes": LAYOUT_CELL_BYTES[layout],
+                    "fp64_equivalent_GBps": nbytes_f64 / args.steps / (avg_launch_ms / 1e3) / 1e9,
+                    "peak_source": peak_src,
                     "kernel": "count_tma_kernel (fused Eq. 1 epilogue)",
                     "avg_launch_us": avg_launch_ms * 1e3}
         line = {

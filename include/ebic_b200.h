@@ -128,6 +128,12 @@ int ebic_evaluate_population(ebic_ctx* ctx, const size_t* offsets, const uint16_
 double ebic_fitness_score(uint64_t match_count, size_t series_len, uint64_t sigma);
 uint64_t ebic_default_sigma(size_t n_rows);
 
+/* Eq. 1 for a whole population on the host: fitness_out[p] =
+ * fitness_score(counts[p], offsets[p+1] - offsets[p], sigma).  Used after a
+ * cross-process all-reduce of shard counts. */
+int ebic_fitness_scores_host(const uint64_t* counts, const size_t* offsets, size_t n_series,
+                             uint64_t sigma, double* fitness_out);
+
 /* Device-pointer variants (single-shard contexts) for callers that keep the
  * CBF in HBM and own the stream (cudaStream_t passed as void*, used as is:
  * NULL is the legacy default stream, as everywhere in CUDA).  d_offsets: uint64[P+1]; d_cols: uint16[offsets[P]];

@@ -51,6 +51,7 @@ SIGNATURES = [
     ("ebic_evaluate_population", C.c_int, [vp, szp, u16p, C.c_size_t, C.c_uint64, C.c_double, u64p, f64p]),
     ("ebic_fitness_score", C.c_double, [C.c_uint64, C.c_size_t, C.c_uint64]),
     ("ebic_default_sigma", C.c_uint64, [C.c_size_t]),
+    ("ebic_fitness_scores_host", C.c_int, [u64p, szp, C.c_size_t, C.c_uint64, f64p]),
     ("ebic_count_matches_device", C.c_int, [vp, vp, vp, C.c_size_t, C.c_size_t, C.c_double, C.c_uint64, vp, vp, vp]),
     ("ebic_fitness_device", C.c_int, [vp, vp, vp, C.c_size_t, C.c_uint64, vp, vp]),
     ("ebic_ctx_phase_times", C.c_int, [vp, u64p, C.c_size_t, szp]),

@@ -887,6 +887,15 @@ double ebic_fitness_score(uint64_t match_count, size_t series_len, uint64_t sigm
     return f > 0.0 ? f : 0.0;
 }
 
+int ebic_fitness_scores_host(const uint64_t* counts, const size_t* offsets, size_t n_series,
+                             uint64_t sigma, double* fitness_out) {
+    return guarded([&] {
+        if (n_series && (!counts || !offsets || !fitness_out)) fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+        for (size_t p = 0; p < n_series; ++p)
+            fitness_out[p] = ebic_fitness_score(counts[p], offsets[p + 1] - offsets[p], sigma);
+    });
+}
+
 uint64_t ebic_default_sigma(size_t n_rows) {
     const uint64_t scaled = static_cast<uint64_t>((n_rows + 49) / 50);  // fitness.hpp:48-52
     return scaled < 4 ? 4 : scaled;
