@@ -21,7 +21,8 @@ from typing import Iterable, List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (CtxInfo, EbicError, check, f64p, lib, ptr, szp, u8p, u16p, u64p)
+from ._lib import (CtxInfo, EbicError, check, f64p, fast_count, fast_evaluate, lib, ptr, szp,
+                   u8p, u16p, u64p)
 
 __all__ = [
     "ExpressionMatrix", "CbfPopulation", "ColumnSeries", "RowRange", "ChunkPlan", "FitnessParams",
@@ -203,11 +204,17 @@ def device_count() -> int:
     return n.value
 
 
+_ONE_COL = np.zeros(1, dtype=np.uint16)
+
+
 def _as_cbf_arrays(pop: CbfPopulation):
-    off = np.ascontiguousarray(pop.offsets, dtype=np.uint64)
-    cols = np.ascontiguousarray(pop.col_indices, dtype=np.uint16)
+    off, cols = pop.offsets, pop.col_indices
+    if off.dtype != np.uint64 or not off.flags.c_contiguous:
+        off = np.ascontiguousarray(off, dtype=np.uint64)
+    if cols.dtype != np.uint16 or not cols.flags.c_contiguous:
+        cols = np.ascontiguousarray(cols, dtype=np.uint16)
     if cols.size == 0:
-        cols = np.zeros(1, dtype=np.uint16)
+        cols = _ONE_COL
     return off, cols
 
 
@@ -299,26 +306,30 @@ class Evaluator:
 
     # -- fitness.hpp:100-118 ------------------------------------------------
     def count_matches(self, pop: CbfPopulation, epsilon: float = 0.0) -> np.ndarray:
-        n = pop.size()
-        out = np.zeros(n, dtype=np.uint64)
-        if n == 0:
-            return out
         off, cols = _as_cbf_arrays(pop)
-        check(lib.ebic_count_matches(self._ctx, ptr(off, szp), ptr(cols, u16p), n, float(epsilon),
-                                     ptr(out, u64p)))
+        n = len(off) - 1
+        out = np.empty(max(n, 0), dtype=np.uint64)
+        if n <= 0:
+            return out
+        rc = fast_count(self._ctx, off.ctypes.data, cols.ctypes.data, n, float(epsilon),
+                        out.ctypes.data)
+        if rc:
+            check(rc)
         return out
 
     # -- fitness.hpp:135-143 ------------------------------------------------
     def evaluate_population(self, pop: CbfPopulation, params: FitnessParams,
                             epsilon: float = 0.0, return_counts: bool = False):
-        n = pop.size()
-        fit = np.zeros(n, dtype=np.float64)
-        counts = np.zeros(n, dtype=np.uint64)
+        off, cols = _as_cbf_arrays(pop)
+        n = max(len(off) - 1, 0)
+        fit = np.empty(n, dtype=np.float64)
+        counts = np.empty(n, dtype=np.uint64) if return_counts else None
         if n:
-            off, cols = _as_cbf_arrays(pop)
-            check(lib.ebic_evaluate_population(self._ctx, ptr(off, szp), ptr(cols, u16p), n,
-                                               int(params.sigma), float(epsilon),
-                                               ptr(counts, u64p), ptr(fit, f64p)))
+            rc = fast_evaluate(self._ctx, off.ctypes.data, cols.ctypes.data, n, int(params.sigma),
+                               float(epsilon), counts.ctypes.data if return_counts else None,
+                               fit.ctypes.data)
+            if rc:
+                check(rc)
         return (fit, counts) if return_counts else fit
 
     # -- membership (expansion.hpp:16-87) ------------------------------------

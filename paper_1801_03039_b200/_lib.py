@@ -87,6 +87,21 @@ def _load() -> C.CDLL:
 lib = _load()
 
 
+def _fast(name, res, args):
+    """A second handle on an entry point with raw-address (c_void_p) pointer
+    arguments: the per-generation hot calls pass ndarray.ctypes.data ints
+    instead of building ctypes pointer objects."""
+    fn = getattr(C.CDLL(str(LIB_PATH)), name)
+    fn.restype = res
+    fn.argtypes = args
+    return fn
+
+
+fast_evaluate = _fast("ebic_evaluate_population", C.c_int,
+                      [vp, vp, vp, C.c_size_t, C.c_uint64, C.c_double, vp, vp])
+fast_count = _fast("ebic_count_matches", C.c_int, [vp, vp, vp, C.c_size_t, C.c_double, vp])
+
+
 class EbicError(RuntimeError):
     """A failed C-ABI call (CUDA failure, no device)."""
 

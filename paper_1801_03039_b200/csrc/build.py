@@ -18,6 +18,8 @@ REPO = PKG.parent
 LIB = PKG / "libebic_b200.so"
 SOURCES = [CSRC / "ebic_b200.cu", CSRC / "synth.cpp"]
 DEPS = SOURCES + [CSRC / "kernels.cuh", REPO / "include" / "ebic_b200.h"]
+E2E = PKG / "ebic_e2e_driver"
+E2E_SRC = CSRC / "e2e_driver.cu"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -29,7 +31,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",
 
 
 def needs_build() -> bool:
-    if not LIB.exists():
+    if not LIB.exists() or not E2E.exists() or E2E_SRC.stat().st_mtime > E2E.stat().st_mtime:
         return True
     t = LIB.stat().st_mtime
     return any(p.stat().st_mtime > t for p in DEPS)
@@ -44,7 +46,18 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True, cwd=str(PKG))
     os.replace(tmp, LIB)
+    build_e2e(verbose)
     return LIB
+
+
+def build_e2e(verbose: bool = False) -> Path:
+    """C++ caller of the public C ABI used by bench.py for the e2e figure."""
+    cmd = [NVCC, *ARCH, "-O3", "-std=c++17", "-o", str(E2E), str(E2E_SRC), "-L", str(PKG),
+           "-lebic_b200", "-Xlinker", "-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, cwd=str(PKG))
+    return E2E
 
 
 def ptxas_report() -> str:

@@ -151,12 +151,17 @@ struct Shard {
     size_t d_out_cap = 0;
     unsigned char* h_pin = nullptr;
     size_t h_pin_cap = 0;
+    // mapped pinned results of host-path launches: [flag (128 B)][counts P][fitness P]
+    unsigned char* h_map = nullptr;
+    size_t h_map_cap = 0;
+    unsigned long long seq = 0;
     Tables tables;
     unsigned long long* d_phase = nullptr;  // EBIC_PHASE_TIMING: per-CTA phase stamps
     RankLayout ranks[2];
     uint64_t rank_clock = 0;
     int has_nan = -1;  // -1 unknown
     int last_grid = 0;
+    int last_reduce = -1;  // reduction-tail mode of the last launch
     CountConfig last_cfg;
 };
 
@@ -170,6 +175,18 @@ void grow_device(unsigned char** p, size_t* cap, size_t need) {
     *cap = n;
 }
 
+// Host memory the device writes directly (zero-copy results + completion flag).
+void grow_mapped(unsigned char** p, size_t* cap, size_t need) {
+    if (need <= *cap) return;
+    if (*p) CK(cudaFreeHost(*p));
+    *p = nullptr;
+    size_t n = std::max(need, *cap * 2);
+    n = (n + 255) & ~size_t(255);
+    CK(cudaHostAlloc(reinterpret_cast<void**>(p), n, cudaHostAllocMapped));
+    std::memset(*p, 0, n);
+    *cap = n;
+}
+
 void grow_pinned(unsigned char** p, size_t* cap, size_t need) {
     if (need <= *cap) return;
     if (*p) CK(cudaFreeHost(*p));
@@ -180,15 +197,26 @@ void grow_pinned(unsigned char** p, size_t* cap, size_t need) {
     *cap = n;
 }
 
-// Reduction scratch of one count launch: (grid + groups) rows of P counters.
-void ensure_partial(Shard& s, size_t P, int grid) {
+// Reduction scratch of one count launch: striped accumulators [P][kStripes]
+// (zero between launches) or the tree's (grid + groups) rows of P counters.
+void ensure_partial(Shard& s, size_t P, int grid, bool striped) {
     const size_t gsz = reduce_group_size((uint32_t)grid);
-    const size_t need = (size_t(grid) + (grid + gsz - 1) / gsz) * P;
-    if (need <= s.partial_cap) return;
+    const size_t need = striped ? P * kStripes : (size_t(grid) + (grid + gsz - 1) / gsz) * P;
+    const int mode = striped ? 1 : 0;
+    if (need <= s.partial_cap && mode == s.last_reduce) return;
+    s.last_reduce = mode;
+    if (need <= s.partial_cap) {  // mode switch: the tree leaves non-zero rows behind
+        CK(cudaMemsetAsync(s.d_partial, 0, s.partial_cap * sizeof(uint32_t), s.stream));
+        CK(cudaStreamSynchronize(s.stream));
+        return;
+    }
     if (s.d_partial) CK(cudaFree(s.d_partial));
     s.d_partial = nullptr;
     const size_t n = std::max(need, s.partial_cap * 2);
     CK(cudaMalloc(&s.d_partial, n * sizeof(uint32_t)));
+    // the striped tail expects zeros and leaves zeros behind
+    CK(cudaMemsetAsync(s.d_partial, 0, n * sizeof(uint32_t), s.stream));
+    CK(cudaStreamSynchronize(s.stream));
     s.partial_cap = n;
 }
 
@@ -517,7 +545,8 @@ const Tables& ensure_tables(Shard& s, uint64_t sigma, size_t total_rows) {
 // Launches the count kernel for one shard.  All pointers are device pointers.
 void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t* d_cols, size_t P,
                   size_t L, double eps, uint64_t* d_counts, double* d_fit, uint64_t sigma,
-                  cudaStream_t st, uint64_t cols_base) {
+                  cudaStream_t st, uint64_t cols_base, unsigned long long* done_flag = nullptr,
+                  unsigned long long done_seq = 0) {
     if (P == 0) return;
     if (P > 0xffffffffull || L > 0xffffffffull || s.rows > 0xffffffffull)
         fail(EBIC_ERR_INVALID_ARGUMENT, "population or shard too large for one launch");
@@ -538,6 +567,9 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
     p.cols_base = cols_base;
     p.sched_static = (uint32_t)env_int("EBIC_SCHED_STATIC", 0);
     p.max_parts = (uint32_t)env_int("EBIC_MAX_PARTS", 8);
+    p.reduce_striped = env_int("EBIC_REDUCE_TREE", 0) ? 0u : 1u;
+    p.done_flag = done_flag;
+    p.done_seq = done_seq;
     p.phase_ns = s.d_phase;
     if (d_fit) {
         const Tables& t = ensure_tables(s, sigma, ctx.total_rows);
@@ -559,7 +591,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         if (g_env > 0) grid = std::min<int>(g_env, (int)p.n_tiles);
         s.last_grid = grid;
         s.last_cfg = c;
-        ensure_partial(s, P, grid);
+        ensure_partial(s, P, grid, p.reduce_striped != 0);
         p.partial = s.d_partial;
         const CUtensorMap& tm = c.layout ? rank_tensor_map(*rl, s, ctx.n_cols, c) : tensor_map(s, ctx.n_cols, c);
         launch_tma(c, e0, tm, p, grid, smem, st);
@@ -569,7 +601,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         const int grid = (int)((s.rows + 255) / 256);
         s.last_grid = grid;
         s.last_cfg = c;
-        ensure_partial(s, P, grid);
+        ensure_partial(s, P, grid, p.reduce_striped != 0);
         p.partial = s.d_partial;
         if (e0) {
             CK(cudaFuncSetAttribute(count_direct_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -599,7 +631,26 @@ void validate_cbf(const size_t* off, const uint16_t* cols, size_t P, size_t n_co
 }
 
 // Packs the CBF into pinned memory, copies it to every shard, launches the
-// count kernel per shard and brings counts (and fitness) back.
+// count kernel per shard; the kernel's final CTA writes counts (and fitness)
+// straight into mapped pinned host memory and raises a completion flag, which
+// the host polls -- no device-to-host copy and no stream synchronisation on
+// the per-generation path (cudaStreamQuery is consulted while polling so a
+// failed launch surfaces as an error instead of a hang).
+void wait_flag(Shard& s, unsigned long long seq) {
+    volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(s.h_map);
+    for (uint64_t spin = 0;; ++spin) {
+        if (*flag == seq) return;
+        if ((spin & 1023) == 1023) {
+            const cudaError_t e = cudaStreamQuery(s.stream);
+            if (e == cudaSuccess) {
+                if (*flag == seq) return;
+                fail(EBIC_ERR_CUDA, "count kernel finished without its completion flag");
+            }
+            if (e != cudaErrorNotReady) cuda_check(e, "count kernel");
+        }
+    }
+}
+
 void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_t P, double eps,
                    bool want_fit, uint64_t sigma, uint64_t* counts_out, double* fit_out) {
     if (P == 0) return;
@@ -608,44 +659,45 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
     const size_t off_bytes = (P + 1) * sizeof(uint64_t);
     const size_t cols_at = (off_bytes + 15) & ~size_t(15);
     const size_t in_bytes = cols_at + L * sizeof(uint16_t);
-    const size_t out_bytes = P * sizeof(uint64_t) * 2;
     const bool single = ctx.shards.size() == 1;
     for (Shard& s : ctx.shards) {
         DeviceGuard g(s.device);
-        grow_pinned(&s.h_pin, &s.h_pin_cap, in_bytes + out_bytes + 16);
+        grow_pinned(&s.h_pin, &s.h_pin_cap, in_bytes + 16);
+        grow_mapped(&s.h_map, &s.h_map_cap, 128 + P * 16);
         grow_device(&s.d_in, &s.d_in_cap, in_bytes + 64);
-        grow_device(&s.d_out, &s.d_out_cap, out_bytes);
         static_assert(sizeof(size_t) == sizeof(uint64_t), "size_t must be 64-bit");
         std::memcpy(s.h_pin, off, off_bytes);
         if (L) std::memcpy(s.h_pin + cols_at, cols, L * sizeof(uint16_t));
         CK(cudaMemcpyAsync(s.d_in, s.h_pin, in_bytes, cudaMemcpyHostToDevice, s.stream));
-        uint64_t* d_counts = reinterpret_cast<uint64_t*>(s.d_out);
-        double* d_fit = (single && want_fit) ? reinterpret_cast<double*>(s.d_out + P * 8) : nullptr;
+        uint64_t* m_counts = reinterpret_cast<uint64_t*>(s.h_map + 128);
+        double* m_fit = (single && want_fit) ? reinterpret_cast<double*>(s.h_map + 128 + P * 8) : nullptr;
         const auto* d_off = reinterpret_cast<const uint64_t*>(s.d_in);
         const auto* d_cols = reinterpret_cast<const uint16_t*>(s.d_in + cols_at);
+        const unsigned long long seq = ++s.seq;
         // One launch per slice of at most kMaxSeriesPerLaunch series /
         // kMaxLenPerLaunch columns (the per-CTA work list lives in shared
-        // memory); a generation (P ~ 600) is always a single launch.
+        // memory); a generation (P ~ 600) is always a single launch.  Only
+        // the last launch raises the flag (launches are stream-ordered).
         for (size_t s0 = 0; s0 < P;) {
             size_t s1 = s0;
             while (s1 < P && s1 - s0 < kMaxSeriesPerLaunch && off[s1 + 1] - off[s0] <= kMaxLenPerLaunch) ++s1;
             if (s1 == s0) s1 = s0 + 1;  // a single over-long series still gets its own launch
-            launch_count(ctx, s, d_off + s0, d_cols, s1 - s0, off[s1] - off[s0], eps, d_counts + s0,
-                         d_fit ? d_fit + s0 : nullptr, sigma, s.stream, off[s0]);
+            const bool last = s1 == P;
+            launch_count(ctx, s, d_off + s0, d_cols, s1 - s0, off[s1] - off[s0], eps, m_counts + s0,
+                         m_fit ? m_fit + s0 : nullptr, sigma, s.stream, off[s0],
+                         last ? reinterpret_cast<unsigned long long*>(s.h_map) : nullptr, seq);
             s0 = s1;
         }
-        CK(cudaMemcpyAsync(s.h_pin + in_bytes, s.d_out, d_fit ? out_bytes : P * 8,
-                           cudaMemcpyDeviceToHost, s.stream));
     }
     std::vector<uint64_t> total;
     if (!single) total.assign(P, 0);
     for (Shard& s : ctx.shards) {
         DeviceGuard g(s.device);
-        CK(cudaStreamSynchronize(s.stream));
-        const uint64_t* c = reinterpret_cast<const uint64_t*>(s.h_pin + in_bytes);
+        wait_flag(s, s.seq);
+        const uint64_t* c = reinterpret_cast<const uint64_t*>(s.h_map + 128);
         if (single) {
             if (counts_out) std::memcpy(counts_out, c, P * 8);
-            if (want_fit) std::memcpy(fit_out, s.h_pin + in_bytes + P * 8, P * 8);
+            if (want_fit) std::memcpy(fit_out, s.h_map + 128 + P * 8, P * 8);
         } else {
             for (size_t p = 0; p < P; ++p) total[p] += c[p];  // exact integer reduction
         }
@@ -718,6 +770,7 @@ void free_shard(Shard& s) {
     cudaFree(s.d_done);
     cudaFree(s.d_out);
     if (s.h_pin) cudaFreeHost(s.h_pin);
+    if (s.h_map) cudaFreeHost(s.h_map);
     cudaFree(s.tables.d_log);
     cudaFree(s.tables.d_exp);
     for (RankLayout& rl : s.ranks) cudaFree(rl.d);

@@ -159,6 +159,12 @@ struct CountParams {
     uint64_t cols_base;                    // == offsets[0] (host-known; no dependent load)
     uint32_t sched_static;                 // debug: static chunk assignment
     uint32_t max_parts;                    // tail split of the last wave (1 = off)
+    uint32_t reduce_striped;               // 1: striped-accumulator tail, 0: reduction tree
+    // Optional completion signal for host callers: after the final CTA has
+    // written counts/fitness (which may live in mapped host memory), it makes
+    // them system-visible and stores done_seq to *done_flag.
+    unsigned long long* done_flag;
+    unsigned long long done_seq;
     unsigned long long* __restrict__ phase_ns;  // optional [grid][8] %globaltimer stamps
 };
 
@@ -418,8 +424,66 @@ __device__ __forceinline__ uint64_t sum_rows(const uint32_t* rows, size_t P, uin
 // every ticket counter is left at zero for the next launch.  Integer sums:
 // the result does not depend on arrival order (fitness.hpp:17-19).
 // `slot_series` maps a counter slot to its series id (nullptr = identity).
+// Striped-accumulator tail (default): every CTA adds its per-series partial
+// counts with fire-and-forget reductions into stripe (blockIdx % kStripes) of
+// a [P][kStripes] u32 accumulator (the eight stripes of a series share one
+// 32-byte sector), so each address sees ~G/8 reductions instead of G; one
+// acq_rel ticket per CTA; the last CTA sums the stripes (one 32-byte load per
+// series), re-zeroes them for the next launch and writes counts + Eq. 1.
+constexpr int kStripes = 8;
+
+// Completion signal of the final CTA (see CountParams::done_flag): the
+// barrier orders every thread's output stores before thread 0's system-scope
+// fence, which makes them visible to the host before the flag.
+__device__ __forceinline__ void signal_done(const CountParams& p) {
+    if (!p.done_flag) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile unsigned long long*>(p.done_flag) = p.done_seq;
+    }
+}
+
+__device__ __forceinline__ void count_epilogue_striped(const CountParams& p, const uint32_t* s_cnt,
+                                                       const uint32_t* slot_series) {
+    const uint32_t P = p.n_series;
+    uint32_t* acc = p.partial;  // [P][kStripes]
+    const uint32_t stripe = blockIdx.x % kStripes;
+    unsigned long long* stamp = p.phase_ns ? p.phase_ns + 8ull * blockIdx.x : nullptr;
+    __shared__ int s_last;
+    for (uint32_t g = threadIdx.x; g < P; g += blockDim.x) {
+        const uint32_t c = s_cnt[g];
+        const uint32_t s = slot_series ? slot_series[g] : g;
+        if (c) atomicAdd(acc + size_t(s) * kStripes + stripe, c);
+    }
+    __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[4] = global_ns();
+    if (threadIdx.x == 0) s_last = ticket_acq_rel(&p.done[kMaxGroups]) == gridDim.x - 1;
+    __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[5] = global_ns();
+    if (!s_last) return;
+    if (stamp && threadIdx.x == 0) stamp[7] = global_ns();
+    for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
+        uint4* a = reinterpret_cast<uint4*>(acc + size_t(s) * kStripes);
+        const uint4 x = __ldcg(a), y = __ldcg(a + 1);
+        const uint64_t c = uint64_t(x.x) + x.y + x.z + x.w + y.x + y.y + y.z + y.w;
+        a[0] = make_uint4(0, 0, 0, 0);
+        a[1] = make_uint4(0, 0, 0, 0);
+        p.counts_out[s] = c;
+        if (p.fitness_out)
+            p.fitness_out[s] = fitness_from_tables(c, p.offsets[s + 1] - p.offsets[s], p.sigma,
+                                                   p.logt, p.expt);
+    }
+    if (threadIdx.x == 0) p.done[kMaxGroups] = 0u;
+    signal_done(p);
+}
+
 __device__ __forceinline__ void count_epilogue(const CountParams& p, const uint32_t* s_cnt,
                                                const uint32_t* slot_series) {
+    if (p.reduce_striped) {
+        count_epilogue_striped(p, s_cnt, slot_series);
+        return;
+    }
     const uint32_t P = p.n_series, G = gridDim.x;
     const uint32_t gsz = reduce_group_size(G);
     const uint32_t n_groups = (G + gsz - 1) / gsz;
@@ -461,6 +525,7 @@ __device__ __forceinline__ void count_epilogue(const CountParams& p, const uint3
                                                    p.logt, p.expt);
     }
     if (threadIdx.x == 0) p.done[kMaxGroups] = 0u;
+    signal_done(p);
 }
 
 // ---------------------------------------------------------------------------
