@@ -575,6 +575,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         const Tables& t = ensure_tables(s, sigma, ctx.total_rows);
         p.logt = t.d_log;
         p.expt = t.d_exp;
+        p.table_n = t.n;
     }
     const bool e0 = (eps == 0.0);
     RankLayout* rl = ensure_ranks(s, ctx.n_cols, eps);

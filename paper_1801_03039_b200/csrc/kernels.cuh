@@ -165,6 +165,7 @@ struct CountParams {
     // them system-visible and stores done_seq to *done_flag.
     unsigned long long* done_flag;
     unsigned long long done_seq;
+    uint64_t table_n;                      // entries of logt/expt (prefetched into L2)
     unsigned long long* __restrict__ phase_ns;  // optional [grid][8] %globaltimer stamps
 };
 
@@ -177,29 +178,24 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // Shared-memory work list of one count launch (P series, L column entries):
 //   s_sl     u32[P]   slot -> series id (slots are length-sorted)
 //   s_slen   u32[P]   slot -> series length
-//   s_sstart u32[P]   slot -> first entry in s_pcols (multiple of 8)
+//   s_sstart u32[P]   slot -> first entry in s_pcols (multiple of 4)
 //   s_cnt    u32[P]   slot -> per-CTA match count
 //   s_rel    u32[P+1] series offsets relative to offsets[0] (prologue scratch)
-//   s_pcols  u16[L + 7P] column lists, each padded to a multiple of 8 entries
-//                     (16-byte aligned: one LDS.128 fetches 8 column indices)
-//   s_raw    u16[L]   the launch's column indices (prologue scratch)
-//   s_hist   u32[kLenBuckets], s_wsum u32[32]
-// The column-list area doubles as scratch for the stable scatter's per-block
-// bucket counts ([ceil(P/32)][kLenBuckets] u32), so it is at least that big.
-__host__ __device__ inline size_t pcols_area_bytes(uint32_t P, uint32_t L) {
-    const size_t cols = 2ull * (L + 7ull * P) + 16;
-    const size_t scratch = 4ull * kLenBuckets * ((P + 31) / 32);
-    return cols > scratch ? cols : scratch;
-}
-
+//   s_pcols  u16[L + 3P] column lists, each padded to a multiple of 4 entries
+//                     (8-byte aligned: one LDS.64 fetches 4 column indices)
+//   s_raw    u16[L+16] the launch's column indices (prologue scratch)
+//   s_wh     u32[ceil(P/32)][kLenBuckets] per-block bucket counts (scratch)
+//   s_hist   u32[kLenBuckets] bucket starts, s_hpad u32[kLenBuckets] bucket
+//            column-list starts, s_wsum u32[32]
 __host__ __device__ inline size_t count_meta_bytes(uint32_t P, uint32_t total_len) {
     size_t b = 16ull * P + 4ull * (P + 1);
     b = (b + 15) & ~size_t(15);
-    b += pcols_area_bytes(P, total_len);
+    b += 2ull * (total_len + 3ull * P) + 16;
     b = (b + 15) & ~size_t(15);
     b += 2ull * total_len + 32;
     b = (b + 15) & ~size_t(15);
-    return b + 4ull * kLenBuckets + 4ull * 32 + 16;
+    b += 4ull * kLenBuckets * ((P + 31) / 32);
+    return b + 4ull * kLenBuckets * 2 + 4ull * 32 + 16;
 }
 
 struct WorkList {
@@ -210,7 +206,9 @@ struct WorkList {
     uint32_t* rel;
     uint16_t* pcols;
     uint16_t* raw;
+    uint32_t* wh;
     uint32_t* hist;
+    uint32_t* hpad;
     uint32_t* wsum;
 };
 
@@ -227,14 +225,15 @@ __device__ __forceinline__ WorkList carve_work_list(unsigned char* p, uint32_t P
     w.sstart = w.slen + P;
     w.cnt = w.sstart + P;
     w.rel = w.cnt + P;
-    size_t off = 16ull * P + 4ull * (P + 1);
-    unsigned char* q = align16(p, off);
+    unsigned char* q = align16(p, 16ull * P + 4ull * (P + 1));
     w.pcols = reinterpret_cast<uint16_t*>(q);
-    q = align16(q, pcols_area_bytes(P, L));
+    q = align16(q, 2ull * (L + 3ull * P) + 16);
     w.raw = reinterpret_cast<uint16_t*>(q);
     q = align16(q, 2ull * L + 32);
-    w.hist = reinterpret_cast<uint32_t*>(q);
-    w.wsum = w.hist + kLenBuckets;
+    w.wh = reinterpret_cast<uint32_t*>(q);
+    w.hist = w.wh + kLenBuckets * ((P + 31) / 32);
+    w.hpad = w.hist + kLenBuckets;
+    w.wsum = w.hpad + kLenBuckets;
     return w;
 }
 
@@ -273,21 +272,48 @@ __device__ __forceinline__ void block_exclusive_scan(uint32_t P, F vals, uint32_
     }
 }
 
-// Cooperative construction of the work list by `nthreads` threads.  One
-// round trip to global memory (offsets + column indices, coalesced), then
-// shared memory only: series are bucket-sorted by length (so the lane groups
-// of one warp walk equally long series) and each series' columns are copied
-// to a padded, 16-byte aligned slot (pad entries hold column 0, a valid
-// address).  Runs while the producer's first TMA stages are in flight.
+__device__ __forceinline__ uint32_t pad4(uint32_t len) { return (len + 3u) & ~3u; }
+
+// Exclusive warp scan of two 64-entry arrays (a: counts, b: weights), lane l
+// owning entries l and l + 32.  Returns the totals through *ta.
+__device__ __forceinline__ void warp_scan64(uint32_t* a, uint32_t* b, int lane) {
+    uint32_t a0 = a[lane], a1 = a[lane + 32], b0 = b[lane], b1 = b[lane + 32];
+    uint32_t x0 = a0, x1 = a1, y0 = b0, y1 = b1;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u0 = __shfl_up_sync(0xffffffffu, x0, o), u1 = __shfl_up_sync(0xffffffffu, x1, o);
+        const uint32_t v0 = __shfl_up_sync(0xffffffffu, y0, o), v1 = __shfl_up_sync(0xffffffffu, y1, o);
+        if (lane >= o) x0 += u0, x1 += u1, y0 += v0, y1 += v1;
+    }
+    const uint32_t tx = __shfl_sync(0xffffffffu, x0, 31), ty = __shfl_sync(0xffffffffu, y0, 31);
+    a[lane] = x0 - a0;
+    a[lane + 32] = tx + x1 - a1;
+    b[lane] = y0 - b0;
+    b[lane + 32] = ty + y1 - b1;
+}
+
+// Cooperative construction of the work list by `nthreads` threads (5 barriers).
+//  A  one round trip to global memory: offsets + column words, coalesced.
+//  B  per 32-series block: bucket (= length, lengths >= 63 share bucket 63),
+//     __match_any_sync peers; block-bucket counts and bucket totals.
+//  C  warp 0: bucket starts and column-list starts (within buckets < 63 all
+//     lists have the same padded length); 64 other threads: per-bucket
+//     exclusive scan over blocks.
+//  D  every series gets slot = bucket start + earlier blocks + rank in block
+//     -- a stable counting sort, so every CTA derives the same slot order (a
+//     chunk range names the same series on every CTA; tail-split tiles rely
+//     on it) -- and copies its columns into its padded list.
+//  E  (only if some series is >= 63 long) list starts of the overflow bucket.
+// Runs while the producer's first TMA stages are in flight.
 __device__ __forceinline__ void build_work_list(const CountParams& p, const WorkList& w, int tid,
                                                 int nthreads, int bar_id) {
     const uint32_t P = p.n_series, L = p.total_len;
+    const uint32_t nblk = (P + 31) / 32;
+    const int lane = tid & 31, nw = nthreads >> 5;
     // A launch may cover a slice of a larger population: column positions are
     // taken relative to offsets[0] (== cols_base, passed by value so the loads
     // below do not wait on it).  The column indices are fetched as whole
     // 16-byte words from the aligned word containing cols[base]; `shift`
-    // re-bases positions inside w.raw.  Both streams are issued before any
-    // shared-memory store so they share one round trip.
+    // re-bases positions inside w.raw.
     const uint64_t base = p.cols_base;
     const uint16_t* src = p.cols + base;
     const uint32_t shift = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) & 15u) >> 1);
@@ -310,88 +336,83 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
             if (i < n_vec) reinterpret_cast<uint4*>(w.raw)[i] = v[k];
         }
     }
+    for (uint32_t i = tid; i < nblk * kLenBuckets; i += nthreads) w.wh[i] = 0;
     for (int b = tid; b < kLenBuckets; b += nthreads) w.hist[b] = 0;
-    named_bar_sync(bar_id, nthreads);
-    for (uint32_t s = tid; s < P; s += nthreads) {
-        const uint32_t len = w.rel[s + 1] - w.rel[s];
-        atomicAdd(&w.hist[len < kLenBuckets ? len : kLenBuckets - 1], 1u);
+    named_bar_sync(bar_id, nthreads);                                        // 1
+
+    auto bucket_of = [&](uint32_t s, uint32_t& len) -> uint32_t {
+        len = s < P ? w.rel[s + 1] - w.rel[s] : 0u;
+        return s < P ? (len < kLenBuckets ? len : kLenBuckets - 1) : 0xffffu;
+    };
+    for (uint32_t blk = tid >> 5; blk < nblk; blk += nw) {
+        uint32_t len;
+        const uint32_t bkt = bucket_of(blk * 32 + lane, len);
+        const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
+        if (bkt != 0xffffu && lane == __ffs(peers) - 1) {
+            w.wh[blk * kLenBuckets + bkt] = __popc(peers);
+            atomicAdd(&w.hist[bkt], static_cast<uint32_t>(__popc(peers)));
+        }
     }
-    named_bar_sync(bar_id, nthreads);
-    if (tid < 32) {  // exclusive scan of the 64 bucket sizes by one warp
-        const uint32_t a = w.hist[tid], b = w.hist[tid + 32];
-        uint32_t x = a;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (tid >= o) x += y;
+    named_bar_sync(bar_id, nthreads);                                        // 2
+
+    if (tid < 32) {
+        // bucket starts (slots) and list starts (pcols entries); bucket 63's
+        // lists are sized in phase E
+        for (int k = 0; k < 2; ++k) {
+            const int b = tid + 32 * k;
+            w.hpad[b] = b < kLenBuckets - 1 ? w.hist[b] * pad4(b) : 0u;
         }
-        const uint32_t total_a = __shfl_sync(0xffffffffu, x, 31);
-        uint32_t z = b;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
-            if (tid >= o) z += y;
+        __syncwarp();
+        warp_scan64(w.hist, w.hpad, tid);
+    } else if (tid < 32 + kLenBuckets) {
+        const int b = tid - 32;
+        uint32_t run = 0;
+        for (uint32_t blk = 0; blk < nblk; ++blk) {
+            const uint32_t t = w.wh[blk * kLenBuckets + b];
+            w.wh[blk * kLenBuckets + b] = run;
+            run += t;
         }
-        w.hist[tid] = x - a;
-        w.hist[tid + 32] = total_a + z - b;
     }
-    named_bar_sync(bar_id, nthreads);
-    // Deterministic (stable) scatter: within a length bucket the slots follow
-    // series order, so every CTA derives the same slot order and a chunk range
-    // names the same series on every CTA (tail-split tiles are shared between
-    // CTAs by chunk range).  Rank within the bucket = same-bucket series in
-    // earlier 32-series blocks (scanned per bucket) + in-warp rank
-    // (__match_any_sync).  The per-block counts live in the not-yet-built
-    // column-list area.
-    {
-        const uint32_t nblk = (P + 31) / 32;
-        uint32_t* wh = reinterpret_cast<uint32_t*>(w.pcols);  // [nblk][kLenBuckets]
-        const int lane = tid & 31, nw = nthreads >> 5;
-        const uint32_t lt = (1u << lane) - 1u;
-        for (uint32_t i = tid; i < nblk * kLenBuckets; i += nthreads) wh[i] = 0;
-        named_bar_sync(bar_id, nthreads);
-        auto bucket_of = [&](uint32_t s, uint32_t& len) -> uint32_t {
-            len = s < P ? w.rel[s + 1] - w.rel[s] : 0u;
-            return s < P ? (len < kLenBuckets ? len : kLenBuckets - 1) : 0xffffu;
-        };
-        for (uint32_t blk = tid >> 5; blk < nblk; blk += nw) {
-            uint32_t len;
-            const uint32_t bkt = bucket_of(blk * 32 + lane, len);
-            const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
-            if (bkt != 0xffffu && lane == __ffs(peers) - 1) wh[blk * kLenBuckets + bkt] = __popc(peers);
+    named_bar_sync(bar_id, nthreads);                                        // 3
+
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t blk = tid >> 5; blk < nblk; blk += nw) {
+        uint32_t len;
+        const uint32_t s = blk * 32 + lane;
+        const uint32_t bkt = bucket_of(s, len);
+        const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
+        if (bkt == 0xffffu) continue;
+        const uint32_t r = w.wh[blk * kLenBuckets + bkt] + __popc(peers & lt);  // rank in bucket
+        const uint32_t g = w.hist[bkt] + r;
+        w.sl[g] = s;
+        w.slen[g] = len;
+        w.cnt[g] = 0;
+        if (bkt < kLenBuckets - 1) {
+            const uint32_t st = w.hpad[bkt] + r * pad4(len);
+            w.sstart[g] = st;
+            const uint16_t* from = w.raw + w.rel[s];
+            for (uint32_t i = 0; i < pad4(len); ++i) w.pcols[st + i] = i < len ? from[i] : 0;
         }
-        named_bar_sync(bar_id, nthreads);
-        if (tid < kLenBuckets) {
-            uint32_t run = w.hist[tid];
-            for (uint32_t blk = 0; blk < nblk; ++blk) {
-                const uint32_t t = wh[blk * kLenBuckets + tid];
-                wh[blk * kLenBuckets + tid] = run;
-                run += t;
+    }
+    named_bar_sync(bar_id, nthreads);                                        // 4
+
+    const uint32_t ovf = w.hist[kLenBuckets - 1];  // first overflow slot
+    if (ovf < P) {                                                           // E (rare)
+        if (tid == 0) {
+            uint32_t run = w.hpad[kLenBuckets - 1];
+            for (uint32_t g = ovf; g < P; ++g) {
+                w.sstart[g] = run;
+                run += pad4(w.slen[g]);
             }
         }
         named_bar_sync(bar_id, nthreads);
-        for (uint32_t blk = tid >> 5; blk < nblk; blk += nw) {
-            uint32_t len;
-            const uint32_t s = blk * 32 + lane;
-            const uint32_t bkt = bucket_of(s, len);
-            const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
-            if (bkt != 0xffffu) {
-                const uint32_t g = wh[blk * kLenBuckets + bkt] + __popc(peers & lt);
-                w.sl[g] = s;
-                w.slen[g] = len;
-                w.cnt[g] = 0;
-            }
+        for (uint32_t g = ovf + tid; g < P; g += nthreads) {
+            const uint32_t len = w.slen[g], st = w.sstart[g];
+            const uint16_t* from = w.raw + w.rel[w.sl[g]];
+            for (uint32_t i = 0; i < pad4(len); ++i) w.pcols[st + i] = i < len ? from[i] : 0;
         }
+        named_bar_sync(bar_id, nthreads);
     }
-    named_bar_sync(bar_id, nthreads);
-    block_exclusive_scan(P, [&](uint32_t g) { return (w.slen[g] + 7u) & ~7u; }, w.sstart, w.wsum,
-                         tid, nthreads, bar_id);
-    named_bar_sync(bar_id, nthreads);
-    for (uint32_t g = tid; g < P; g += nthreads) {
-        const uint32_t len = w.slen[g], st = w.sstart[g];
-        const uint16_t* src = w.raw + w.rel[w.sl[g]];
-        const uint32_t padded = (len + 7u) & ~7u;
-        for (uint32_t i = 0; i < padded; ++i) w.pcols[st + i] = i < len ? src[i] : 0;
-    }
-    named_bar_sync(bar_id, nthreads);
 }
 
 // Ticket with release (publishes this CTA's prior writes, ordered before it
@@ -562,12 +583,14 @@ struct F64Walker {
     template <int L>
     __device__ __forceinline__ static uint32_t walk_fixed(const unsigned char* base,
                                                           const uint16_t* pc, double eps) {
-        uint32_t w[8];
-        const uint4 q0 = *reinterpret_cast<const uint4*>(pc);
-        w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-        if (L > 8) {
-            const uint4 q1 = *reinterpret_cast<const uint4*>(pc + 8);
-            w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+        uint32_t w[6];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if (4 * q < L) {
+                const uint2 x = *reinterpret_cast<const uint2*>(pc + 4 * q);
+                w[2 * q] = x.x;
+                w[2 * q + 1] = x.y;
+            }
         }
         if (RPL == 1) {
             double prev = *reinterpret_cast<const double*>(base + (col_at(w, 0) << kShift));
@@ -700,12 +723,15 @@ struct RankWalker {
     __device__ __forceinline__ static uint4 ld(const unsigned char* base, uint32_t col) {
         return *reinterpret_cast<const uint4*>(base + (col << kShift));
     }
+    // Column lists are 8-byte aligned (padded to 4 entries): LDS.64 per 4 columns.
     __device__ __forceinline__ static void load_cols(uint32_t* w, const uint16_t* pc, int L) {
-        const uint4 q0 = *reinterpret_cast<const uint4*>(pc);
-        w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-        if (L > 8) {
-            const uint4 q1 = *reinterpret_cast<const uint4*>(pc + 8);
-            w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if (4 * q < L) {
+                const uint2 x = *reinterpret_cast<const uint2*>(pc + 4 * q);
+                w[2 * q] = x.x;
+                w[2 * q + 1] = x.y;
+            }
         }
     }
     // One adjacent pair: ok[k] accumulates bit 15/31 per row.
@@ -731,7 +757,7 @@ struct RankWalker {
     __device__ __forceinline__ static uint32_t count2_fixed(const unsigned char* base,
                                                             const uint16_t* pa, const uint16_t* pb,
                                                             const Mask& vm) {
-        uint32_t wa[8], wb[8];
+        uint32_t wa[6], wb[6];
         load_cols(wa, pa, L);
         load_cols(wb, pb, L);
         uint32_t oka[kWords], okb[kWords];
@@ -865,6 +891,22 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 
     if (warp == NCW) {
         // ---------------- producer warp: TMA ring ----------------
+        if (lane == 1 && p.fitness_out && p.table_n) {
+            // Warm L2 with this CTA's slice of the Eq. 1 tables: the final CTA
+            // looks entries up at arbitrary counts after the last tile.
+            const uint64_t bytes = p.table_n * sizeof(double);
+            const uint64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 127) & ~uint64_t(127);
+            const uint64_t lo = per * blockIdx.x;
+            if (lo < bytes) {
+                const uint32_t n = static_cast<uint32_t>(min(per, bytes - lo) & ~uint64_t(15));
+                if (n) {
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     reinterpret_cast<const unsigned char*>(p.logt) + lo), "r"(n) : "memory");
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     reinterpret_cast<const unsigned char*>(p.expt) + lo), "r"(n) : "memory");
+                }
+            }
+        }
         if (lane == 0) {
             uint32_t st = 0, phase = 0;
             for (uint32_t item = blockIdx.x; item < n_items; item += G) {
