@@ -304,9 +304,13 @@ const CUtensorMap& tensor_map(Shard& s, size_t n_cols, const CountConfig& cfg) {
 }
 
 // Shared-memory bytes of a TMA count launch.
+bool scratch_in_stage(const CountConfig& c, size_t P, size_t L) {
+    return c.stages >= 2 && count_scratch_bytes((uint32_t)P, (uint32_t)L) <= c.stage_bytes;
+}
+
 size_t tma_smem_bytes(const CountConfig& c, size_t P, size_t L) {
-    return 128 + size_t(c.stages) * c.stage_bytes + 2 * kMaxStages * sizeof(uint64_t) +
-           count_meta_bytes((uint32_t)P, (uint32_t)L);
+    return 128 + size_t(c.stages) * c.stage_bytes + (2 * kMaxStages + 2) * sizeof(uint64_t) +
+           count_meta_bytes((uint32_t)P, (uint32_t)L, scratch_in_stage(c, P, L)) + 16;
 }
 
 // Fits a stage ring for a tile of `col_bytes` per column: the deepest ring
@@ -586,6 +590,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         p.stage_bytes = c.stage_bytes;
         p.stages = (uint32_t)c.stages;
         p.n_tiles = (uint32_t)((s.rows + c.rpg - 1) / c.rpg);
+        p.scratch_in_stage = scratch_in_stage(c, P, L) ? 1u : 0u;
         const size_t smem = tma_smem_bytes(c, P, L);
         int grid = std::min<int>((int)p.n_tiles, s.sm_count);
         const int g_env = env_int("EBIC_GRID", 0);

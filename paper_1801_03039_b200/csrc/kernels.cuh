@@ -160,6 +160,7 @@ struct CountParams {
     uint32_t sched_static;                 // debug: static chunk assignment
     uint32_t max_parts;                    // tail split of the last wave (1 = off)
     uint32_t reduce_striped;               // 1: striped-accumulator tail, 0: reduction tree
+    uint32_t scratch_in_stage;             // prologue scratch lives in the last stage buffer
     // Optional completion signal for host callers: after the final CTA has
     // written counts/fitness (which may live in mapped host memory), it makes
     // them system-visible and stores done_seq to *done_flag.
@@ -175,27 +176,30 @@ __device__ __forceinline__ unsigned long long global_ns() {
     return t;
 }
 
-// Shared-memory work list of one count launch (P series, L column entries):
+// Shared-memory work list of one count launch (P series, L column entries).
+// Persistent part (lives through the whole launch):
 //   s_sl     u32[P]   slot -> series id (slots are length-sorted)
 //   s_slen   u32[P]   slot -> series length
 //   s_sstart u32[P]   slot -> first entry in s_pcols (multiple of 4)
 //   s_cnt    u32[P]   slot -> per-CTA match count
-//   s_rel    u32[P+1] series offsets relative to offsets[0] (prologue scratch)
-//   s_pcols  u16[L + 3P] column lists, each padded to a multiple of 4 entries
-//                     (8-byte aligned: one LDS.64 fetches 4 column indices)
-//   s_raw    u16[L+16] the launch's column indices (prologue scratch)
-//   s_wh     u32[ceil(P/32)][kLenBuckets] per-block bucket counts (scratch)
-//   s_hist   u32[kLenBuckets] bucket starts, s_hpad u32[kLenBuckets] bucket
-//            column-list starts, s_wsum u32[32]
-__host__ __device__ inline size_t count_meta_bytes(uint32_t P, uint32_t total_len) {
-    size_t b = 16ull * P + 4ull * (P + 1);
-    b = (b + 15) & ~size_t(15);
-    b += 2ull * (total_len + 3ull * P) + 16;
-    b = (b + 15) & ~size_t(15);
-    b += 2ull * total_len + 32;
-    b = (b + 15) & ~size_t(15);
-    b += 4ull * kLenBuckets * ((P + 31) / 32);
-    return b + 4ull * kLenBuckets * 2 + 4ull * 32 + 16;
+//   s_pcols  u32[L + 3P] per series, the BYTE OFFSETS (column x column-slice
+//                     bytes) of its columns inside a staged tile, padded to a
+//                     multiple of 4 entries: one LDS.128 fetches 4 offsets and
+//                     an element address is a single add.
+// Prologue scratch (dead once the list is built; placed in the last TMA stage
+// buffer, which the producer fills only after the prologue, when it fits):
+//   s_rel u32[P+1], s_raw u16[L+16], s_wh u32[ceil(P/32)][kLenBuckets],
+//   s_hist/s_hpad u32[kLenBuckets], s_wsum u32[32]
+__host__ __device__ inline size_t count_persist_bytes(uint32_t P, uint32_t L) {
+    return ((16ull * P + 15) & ~size_t(15)) + 4ull * (L + 3ull * P) + 16;
+}
+__host__ __device__ inline size_t count_scratch_bytes(uint32_t P, uint32_t L) {
+    size_t b = (4ull * (P + 1) + 15) & ~size_t(15);
+    b += (2ull * L + 32 + 15) & ~size_t(15);
+    return b + 4ull * kLenBuckets * ((P + 31) / 32) + 4ull * kLenBuckets * 2 + 4ull * 32 + 16;
+}
+__host__ __device__ inline size_t count_meta_bytes(uint32_t P, uint32_t L, bool scratch_in_stage) {
+    return count_persist_bytes(P, L) + (scratch_in_stage ? 0 : count_scratch_bytes(P, L) + 16);
 }
 
 struct WorkList {
@@ -203,8 +207,9 @@ struct WorkList {
     uint32_t* slen;
     uint32_t* sstart;
     uint32_t* cnt;
+    uint32_t* pcols;
+    // prologue scratch
     uint32_t* rel;
-    uint16_t* pcols;
     uint16_t* raw;
     uint32_t* wh;
     uint32_t* hist;
@@ -216,18 +221,18 @@ __device__ __forceinline__ unsigned char* align16(unsigned char* base, size_t of
     return base + ((off + 15) & ~size_t(15));
 }
 
-// Carves the work list out of shared memory starting at `p` (16-byte aligned).
-// Pointer arithmetic on the shared window only (keeps LDS/STS addressing).
-__device__ __forceinline__ WorkList carve_work_list(unsigned char* p, uint32_t P, uint32_t L) {
+// Carves the work list: persistent part at `p`, scratch at `q` (both 16-byte
+// aligned).  Pointer arithmetic on the shared window only (LDS/STS addressing).
+__device__ __forceinline__ WorkList carve_work_list(unsigned char* p, unsigned char* q, uint32_t P,
+                                                    uint32_t L) {
     WorkList w;
     w.sl = reinterpret_cast<uint32_t*>(p);
     w.slen = w.sl + P;
     w.sstart = w.slen + P;
     w.cnt = w.sstart + P;
-    w.rel = w.cnt + P;
-    unsigned char* q = align16(p, 16ull * P + 4ull * (P + 1));
-    w.pcols = reinterpret_cast<uint16_t*>(q);
-    q = align16(q, 2ull * (L + 3ull * P) + 16);
+    w.pcols = reinterpret_cast<uint32_t*>(align16(p, 16ull * P));
+    w.rel = reinterpret_cast<uint32_t*>(q);
+    q = align16(q, 4ull * (P + 1));
     w.raw = reinterpret_cast<uint16_t*>(q);
     q = align16(q, 2ull * L + 32);
     w.wh = reinterpret_cast<uint32_t*>(q);
@@ -305,7 +310,7 @@ __device__ __forceinline__ void warp_scan64(uint32_t* a, uint32_t* b, int lane) 
 //  E  (only if some series is >= 63 long) list starts of the overflow bucket.
 // Runs while the producer's first TMA stages are in flight.
 __device__ __forceinline__ void build_work_list(const CountParams& p, const WorkList& w, int tid,
-                                                int nthreads, int bar_id) {
+                                                int nthreads, int bar_id, uint32_t col_bytes) {
     const uint32_t P = p.n_series, L = p.total_len;
     const uint32_t nblk = (P + 31) / 32;
     const int lane = tid & 31, nw = nthreads >> 5;
@@ -391,7 +396,7 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
             const uint32_t st = w.hpad[bkt] + r * pad4(len);
             w.sstart[g] = st;
             const uint16_t* from = w.raw + w.rel[s];
-            for (uint32_t i = 0; i < pad4(len); ++i) w.pcols[st + i] = i < len ? from[i] : 0;
+            for (uint32_t i = 0; i < pad4(len); ++i) w.pcols[st + i] = i < len ? from[i] * col_bytes : 0u;
         }
     }
     named_bar_sync(bar_id, nthreads);                                        // 4
@@ -409,7 +414,7 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
         for (uint32_t g = ovf + tid; g < P; g += nthreads) {
             const uint32_t len = w.slen[g], st = w.sstart[g];
             const uint16_t* from = w.raw + w.rel[w.sl[g]];
-            for (uint32_t i = 0; i < pad4(len); ++i) w.pcols[st + i] = i < len ? from[i] : 0;
+            for (uint32_t i = 0; i < pad4(len); ++i) w.pcols[st + i] = i < len ? from[i] * col_bytes : 0u;
         }
         named_bar_sync(bar_id, nthreads);
     }
@@ -574,75 +579,6 @@ struct F64Walker {
         return m;
     }
 
-    __device__ __forceinline__ static uint32_t col_at(const uint32_t* w, int i) {
-        const uint32_t x = w[i >> 1];
-        return (i & 1) ? (x >> 16) : (x & 0xffffu);
-    }
-
-    // All lane groups of the warp walk series of exactly L columns.
-    template <int L>
-    __device__ __forceinline__ static uint32_t walk_fixed(const unsigned char* base,
-                                                          const uint16_t* pc, double eps) {
-        uint32_t w[6];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            if (4 * q < L) {
-                const uint2 x = *reinterpret_cast<const uint2*>(pc + 4 * q);
-                w[2 * q] = x.x;
-                w[2 * q + 1] = x.y;
-            }
-        }
-        if (RPL == 1) {
-            double prev = *reinterpret_cast<const double*>(base + (col_at(w, 0) << kShift));
-            bool ok = true;
-#pragma unroll
-            for (int i = 1; i < L; ++i) {
-                const double cur = *reinterpret_cast<const double*>(base + (col_at(w, i) << kShift));
-                ok = ok & step_ok<kEpsZero>(prev, cur, eps);
-                prev = cur;
-            }
-            return ok ? 1u : 0u;
-        } else {
-            double2 prev = *reinterpret_cast<const double2*>(base + (col_at(w, 0) << kShift));
-            bool a = true, b = true;
-#pragma unroll
-            for (int i = 1; i < L; ++i) {
-                const double2 cur = *reinterpret_cast<const double2*>(base + (col_at(w, i) << kShift));
-                a = a & step_ok<kEpsZero>(prev.x, cur.x, eps);
-                b = b & step_ok<kEpsZero>(prev.y, cur.y, eps);
-                prev = cur;
-            }
-            return (a ? 1u : 0u) | (b ? 2u : 0u);
-        }
-    }
-
-    // Any length, per-lane trip count (mixed-length warps, long series).
-    __device__ __forceinline__ static uint32_t walk_any(const unsigned char* base,
-                                                        const uint16_t* pc, uint32_t len,
-                                                        double eps) {
-        if (len <= 1) return kAll;  // no adjacent pair: the row matches (fitness.hpp:80-90)
-        if (RPL == 1) {
-            double prev = *reinterpret_cast<const double*>(base + (uint32_t(pc[0]) << kShift));
-            bool ok = true;
-            for (uint32_t i = 1; i < len; ++i) {
-                const double cur = *reinterpret_cast<const double*>(base + (uint32_t(pc[i]) << kShift));
-                ok = ok & step_ok<kEpsZero>(prev, cur, eps);
-                prev = cur;
-            }
-            return ok ? 1u : 0u;
-        } else {
-            double2 prev = *reinterpret_cast<const double2*>(base + (uint32_t(pc[0]) << kShift));
-            bool a = true, b = true;
-            for (uint32_t i = 1; i < len; ++i) {
-                const double2 cur = *reinterpret_cast<const double2*>(base + (uint32_t(pc[i]) << kShift));
-                a = a & step_ok<kEpsZero>(prev.x, cur.x, eps);
-                b = b & step_ok<kEpsZero>(prev.y, cur.y, eps);
-                prev = cur;
-            }
-            return (a ? 1u : 0u) | (b ? 2u : 0u);
-        }
-    }
-
     static constexpr int kSeriesPerGroup = 1;
     __device__ __forceinline__ static uint32_t count_group(const unsigned char* base,
                                                            const WorkList& wl, uint32_t g0,
@@ -653,7 +589,77 @@ struct F64Walker {
         return __popc(walk(base, wl.pcols + wl.sstart[g0], len, uniform, eps) & vm);
     }
 
-    __device__ __forceinline__ static uint32_t walk(const unsigned char* base, const uint16_t* pc,
+    __device__ __forceinline__ static void load_offs(uint32_t* w, const uint32_t* pc, int L) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if (4 * q < L) {
+                const uint4 x = *reinterpret_cast<const uint4*>(pc + 4 * q);
+                w[4 * q] = x.x;
+                w[4 * q + 1] = x.y;
+                w[4 * q + 2] = x.z;
+                w[4 * q + 3] = x.w;
+            }
+        }
+    }
+
+    // All lane groups of the warp walk series of exactly L columns.
+    template <int L>
+    __device__ __forceinline__ static uint32_t walk_fixed(const unsigned char* base,
+                                                          const uint32_t* pc, double eps) {
+        uint32_t w[12];
+        load_offs(w, pc, L);
+        if (RPL == 1) {
+            double prev = *reinterpret_cast<const double*>(base + w[0]);
+            bool ok = true;
+#pragma unroll
+            for (int i = 1; i < L; ++i) {
+                const double cur = *reinterpret_cast<const double*>(base + w[i]);
+                ok = ok & step_ok<kEpsZero>(prev, cur, eps);
+                prev = cur;
+            }
+            return ok ? 1u : 0u;
+        } else {
+            double2 prev = *reinterpret_cast<const double2*>(base + w[0]);
+            bool a = true, b = true;
+#pragma unroll
+            for (int i = 1; i < L; ++i) {
+                const double2 cur = *reinterpret_cast<const double2*>(base + w[i]);
+                a = a & step_ok<kEpsZero>(prev.x, cur.x, eps);
+                b = b & step_ok<kEpsZero>(prev.y, cur.y, eps);
+                prev = cur;
+            }
+            return (a ? 1u : 0u) | (b ? 2u : 0u);
+        }
+    }
+
+    // Any length, per-lane trip count (mixed-length warps, long series).
+    __device__ __forceinline__ static uint32_t walk_any(const unsigned char* base,
+                                                        const uint32_t* pc, uint32_t len,
+                                                        double eps) {
+        if (len <= 1) return kAll;  // no adjacent pair: the row matches (fitness.hpp:80-90)
+        if (RPL == 1) {
+            double prev = *reinterpret_cast<const double*>(base + pc[0]);
+            bool ok = true;
+            for (uint32_t i = 1; i < len; ++i) {
+                const double cur = *reinterpret_cast<const double*>(base + pc[i]);
+                ok = ok & step_ok<kEpsZero>(prev, cur, eps);
+                prev = cur;
+            }
+            return ok ? 1u : 0u;
+        } else {
+            double2 prev = *reinterpret_cast<const double2*>(base + pc[0]);
+            bool a = true, b = true;
+            for (uint32_t i = 1; i < len; ++i) {
+                const double2 cur = *reinterpret_cast<const double2*>(base + pc[i]);
+                a = a & step_ok<kEpsZero>(prev.x, cur.x, eps);
+                b = b & step_ok<kEpsZero>(prev.y, cur.y, eps);
+                prev = cur;
+            }
+            return (a ? 1u : 0u) | (b ? 2u : 0u);
+        }
+    }
+
+    __device__ __forceinline__ static uint32_t walk(const unsigned char* base, const uint32_t* pc,
                                                     uint32_t len, bool uniform, double eps) {
         if (uniform) {
             switch (len) {
@@ -716,21 +722,24 @@ struct RankWalker {
                      ((row0 + 2 * k + 1 < n_rows) ? 0x80000000u : 0u);
         return v;
     }
-    __device__ __forceinline__ static uint32_t col_at(const uint32_t* w, int i) {
-        const uint32_t x = w[i >> 1];
-        return (i & 1) ? (x >> 16) : (x & 0xffffu);
+    // 32-bit shared-window address arithmetic: one add per element.
+    __device__ __forceinline__ static uint4 ld(uint32_t base, uint32_t off) {
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(base + off));
+        return v;
     }
-    __device__ __forceinline__ static uint4 ld(const unsigned char* base, uint32_t col) {
-        return *reinterpret_cast<const uint4*>(base + (col << kShift));
-    }
-    // Column lists are 8-byte aligned (padded to 4 entries): LDS.64 per 4 columns.
-    __device__ __forceinline__ static void load_cols(uint32_t* w, const uint16_t* pc, int L) {
+    // Offset lists are 16-byte aligned (padded to 4 entries): LDS.128 per 4.
+    __device__ __forceinline__ static void load_offs(uint32_t* w, const uint32_t* pc, int L) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             if (4 * q < L) {
-                const uint2 x = *reinterpret_cast<const uint2*>(pc + 4 * q);
-                w[2 * q] = x.x;
-                w[2 * q + 1] = x.y;
+                const uint4 x = *reinterpret_cast<const uint4*>(pc + 4 * q);
+                w[4 * q] = x.x;
+                w[4 * q + 1] = x.y;
+                w[4 * q + 2] = x.z;
+                w[4 * q + 3] = x.w;
             }
         }
     }
@@ -754,20 +763,19 @@ struct RankWalker {
     }
     // Two series of exactly L columns, walked interleaved (independent chains).
     template <int L>
-    __device__ __forceinline__ static uint32_t count2_fixed(const unsigned char* base,
-                                                            const uint16_t* pa, const uint16_t* pb,
-                                                            const Mask& vm) {
-        uint32_t wa[6], wb[6];
-        load_cols(wa, pa, L);
-        load_cols(wb, pb, L);
+    __device__ __forceinline__ static uint32_t count2_fixed(uint32_t base, const uint32_t* pa,
+                                                            const uint32_t* pb, const Mask& vm) {
+        uint32_t wa[12], wb[12];
+        load_offs(wa, pa, L);
+        load_offs(wb, pb, L);
         uint32_t oka[kWords], okb[kWords];
 #pragma unroll
         for (int k = 0; k < kWords; ++k) oka[k] = okb[k] = 0xffffffffu;
-        uint4 preva = ld(base, col_at(wa, 0)), prevb = ld(base, col_at(wb, 0));
+        uint4 preva = ld(base, wa[0]), prevb = ld(base, wb[0]);
 #pragma unroll
         for (int i = 1; i < L; ++i) {
-            const uint4 cura = ld(base, col_at(wa, i));
-            const uint4 curb = ld(base, col_at(wb, i));
+            const uint4 cura = ld(base, wa[i]);
+            const uint4 curb = ld(base, wb[i]);
             step(oka, preva, cura);
             step(okb, prevb, curb);
             preva = cura;
@@ -775,9 +783,8 @@ struct RankWalker {
         }
         return tally(oka, vm) | (tally(okb, vm) << 16);
     }
-    __device__ __forceinline__ static uint32_t count_any(const unsigned char* base,
-                                                         const uint16_t* pc, uint32_t len,
-                                                         const Mask& vm) {
+    __device__ __forceinline__ static uint32_t count_any(uint32_t base, const uint32_t* pc,
+                                                         uint32_t len, const Mask& vm) {
         uint32_t ok[kWords];
 #pragma unroll
         for (int k = 0; k < kWords; ++k) ok[k] = 0xffffffffu;
@@ -793,13 +800,14 @@ struct RankWalker {
     }
     // Counts of slots g0 and g0+1 (16-bit fields).  `uniform`: every slot of
     // the warp's chunk exists and has length ulen.
-    __device__ __forceinline__ static uint32_t count_group(const unsigned char* base,
+    __device__ __forceinline__ static uint32_t count_group(const unsigned char* base_ptr,
                                                            const WorkList& wl, uint32_t g0,
                                                            uint32_t P, bool uniform, uint32_t ulen,
                                                            double, const Mask& vm) {
+        const uint32_t base = smem_u32(base_ptr);
         if (uniform) {
-            const uint16_t* pa = wl.pcols + wl.sstart[g0];
-            const uint16_t* pb = wl.pcols + wl.sstart[g0 + 1];
+            const uint32_t* pa = wl.pcols + wl.sstart[g0];
+            const uint32_t* pb = wl.pcols + wl.sstart[g0 + 1];
             switch (ulen) {
                 case 2: return count2_fixed<2>(base, pa, pb, vm);
                 case 3: return count2_fixed<3>(base, pa, pb, vm);
@@ -857,8 +865,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     unsigned char* stage_base = smem;
     uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * p.stage_bytes);
     uint64_t* empty_bar = full_bar + kMaxStages;
-    const WorkList wl = carve_work_list(reinterpret_cast<unsigned char*>(empty_bar + kMaxStages), P,
-                                        p.total_len);
+    uint64_t* prol_bar = empty_bar + kMaxStages;  // work list built (scratch stage released)
+    unsigned char* persist = reinterpret_cast<unsigned char*>(prol_bar + 2);
+    unsigned char* scratch = p.scratch_in_stage
+                                 ? stage_base + size_t(p.stages - 1) * p.stage_bytes
+                                 : align16(persist, count_persist_bytes(P, p.total_len));
+    const WorkList wl = carve_work_list(persist, scratch, P, p.total_len);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -870,6 +882,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], NCW);
         }
+        mbar_init(prol_bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -908,9 +921,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             }
         }
         if (lane == 0) {
-            uint32_t st = 0, phase = 0;
-            for (uint32_t item = blockIdx.x; item < n_items; item += G) {
+            uint32_t st = 0, phase = 0, issued = 0;
+            for (uint32_t item = blockIdx.x; item < n_items; item += G, ++issued) {
                 const uint32_t tile = item < full ? item : full + (item - full) / parts;
+                // the last stage holds the prologue scratch until the work list is built
+                if (p.scratch_in_stage && issued == p.stages - 1) mbar_wait(prol_bar, 0);
                 mbar_wait(&empty_bar[st], phase ^ 1u);
                 s_next[st] = 0;  // published to the consumers by the arrive below (release)
                 mbar_arrive_expect_tx(&full_bar[st], p.stage_bytes);
@@ -924,7 +939,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         }
     } else {
         // ---------------- consumer warps ----------------
-        build_work_list(p, wl, threadIdx.x, NCW * 32, 1);
+        build_work_list(p, wl, threadIdx.x, NCW * 32, 1, Walker::kColBytes);
+        if (threadIdx.x == 0) mbar_arrive(prol_bar);
         if (stamp && threadIdx.x == 0) stamp[1] = global_ns();
 
         const int grp = lane / GL;   // group within warp
