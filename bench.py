@@ -207,6 +207,65 @@ def workload_config(t, args):
 
 
 # ---------------------------------------------------------------------------
+def large_roofline(args, peak):
+    """Roofline of the count kernel on BASELINE config 5 (200,000 x 1000, the
+    scaling-sweep matrix): its tile (800 MB in the rank layout) exceeds the
+    126 MB L2, so back-to-back steps are HBM-cold without eviction and the
+    per-launch host/launch overhead is amortised.  Reported beside the
+    headline C4 line (where one step is ~10 us of HBM time plus a ~5.5 us
+    event/launch floor)."""
+    import torch
+    import paper_1801_03039_b200 as eb
+    from paper_1801_03039_b200 import _lib
+    t = load_workload("c5")
+    values = t.matrix()
+    ev = eb.Evaluator(values)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream(dev)
+    bs = []
+    for off, cols, counts, fit in t.batches:
+        bs.append(dict(P=len(off) - 1, L=int(off[-1]), off_np=off, cols_np=cols, want=counts,
+                       off=torch.from_numpy(off.astype(np.int64)).to(dev),
+                       cols=torch.from_numpy(cols.view(np.int16)).to(dev),
+                       counts=torch.zeros(len(off) - 1, dtype=torch.int64, device=dev),
+                       fit=torch.zeros(len(off) - 1, dtype=torch.float64, device=dev)))
+
+    def step(b):
+        _lib.check(_lib.lib.ebic_count_matches_device(
+            ev.handle, b["off"].data_ptr(), b["cols"].data_ptr(), b["P"], b["L"], t.eps, t.sigma,
+            b["counts"].data_ptr(), b["fit"].data_ptr(), stream.cuda_stream))
+
+    for k in range(4):
+        step(bs[k % len(bs)])
+    torch.cuda.synchronize()
+    for b in bs:
+        step(b)
+        torch.cuda.synchronize()
+        assert (b["counts"].cpu().numpy().astype(np.uint64) == b["want"]).all(), "C5 count mismatch"
+    layout = ev.info().layout
+    nbytes = 0
+    steps = max(20, min(args.steps // 20, 200))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for k in range(steps):
+        b = bs[k % len(bs)]
+        step(b)
+        nbytes += algorithmic_bytes(values.shape[0], b["off_np"], b["cols_np"], LAYOUT_CELL_BYTES[layout])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / steps
+    series = sum(bs[k % len(bs)]["P"] for k in range(steps))
+    achieved = nbytes / steps / (us / 1e6) / 1e9
+    ev.close()
+    return {"workload": "c5: synthetic 200000x1000 (5 planted 6000x30 trend blocks, seed 2026+1), "
+                        "reference GA batches", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "avg_launch_us": us,
+            "algorithmic_bytes_per_launch": nbytes / steps, "layout": LAYOUT_NAMES[layout],
+            "biclusters_per_s": series / (us * steps / 1e6), "steps": steps,
+            "timing": "back-to-back launches between one CUDA event pair (inputs > L2)"}
+
+
 def run_e2e_driver(t, args):
     """Runs paper_1801_03039_b200/ebic_e2e_driver on the workload's batches."""
     import tempfile
@@ -242,9 +301,13 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    sharded = world > 1 or args.force_sharded
+    if sharded:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
@@ -252,7 +315,6 @@ def run_ours(args):
     values = t.matrix()
     R = values.shape[0]
     lo, hi = eb.shard_range(R, world, rank)
-    sharded = world > 1
     if sharded:
         ev = eb.Evaluator(values[lo:hi], devices=[local], shard=(lo, R))
     else:
@@ -418,6 +480,10 @@ def run_ours(args):
         h2d //= args.steps
         d2h //= args.steps
 
+    big = None
+    if not sharded and not args.no_large:
+        ev.close()
+        big = large_roofline(args, peak)
     cb = None
     if rank == 0 and not args.no_cpu_baseline:
         cb = cpu_reference(t, values, t.batches, steps=min(args.steps, 40), warmup=2,
@@ -457,6 +523,7 @@ def run_ours(args):
                                 "d2h_bytes_per_step": d2h,
                                 "caller": "Python Evaluator.evaluate_population (ctypes)"}
                                if e2e_val else None),
+            "roofline_c5": big,
             "gpu_launches": args.steps * launches_per_step,
             "kernel_config": {"rows_per_tile": info.rows_per_tile, "stages": info.stages,
                               "grid": info.grid, "sm_count": info.sm_count,
@@ -480,6 +547,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-large", action="store_true",
+                    help="skip the config-5 (200,000 x 1000) roofline run")
+    ap.add_argument("--force-sharded", action="store_true",
+                    help="use the multi-process shard path (all-reduce + fitness kernel) even at N=1")
     ap.add_argument("--cpu-budget", type=float, default=15.0,
                     help="seconds of timed CPU reference work for cpu_baseline")
     args = ap.parse_args()

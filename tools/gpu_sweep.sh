@@ -5,7 +5,7 @@ out=gpurun_out/sweep.log
 : > $out
 for cfg in "$@"; do
   echo "== $cfg" >> $out
-  env $cfg timeout 300 python bench.py --steps 400 --warmup 5 --no-cpu-baseline ${BENCH_ARGS:-} 2>&1 | \
+  env $cfg timeout 300 python bench.py --steps 400 --warmup 5 --no-cpu-baseline --no-large ${BENCH_ARGS:-} 2>&1 | \
     python -c "import sys,json
 for l in sys.stdin:
     l=l.strip()
