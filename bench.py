@@ -115,8 +115,8 @@ class ClockSampler:
 
 
 # bytes per matrix cell of the layout the count kernel streams (ebic_ctx_info.layout)
-LAYOUT_CELL_BYTES = {0: 8, 1: 2, 2: 4}
-LAYOUT_NAMES = {0: "fp64", 1: "rank16x1", 2: "rank16x2"}
+LAYOUT_CELL_BYTES = {0: 8, 1: 2, 2: 4, 3: 2}
+LAYOUT_NAMES = {0: "fp64", 1: "rank16x1", 2: "rank16x2", 3: "rank16x1c"}
 
 
 def algorithmic_bytes(rows: int, off: np.ndarray, cols: np.ndarray, cell_bytes: int) -> int:
@@ -527,7 +527,7 @@ def run_ours(args):
             "gpu_launches": args.steps * launches_per_step,
             "kernel_config": {"rows_per_tile": info.rows_per_tile, "stages": info.stages,
                               "grid": info.grid, "sm_count": info.sm_count,
-                              "layout": ["fp64", "rank16x1", "rank16x2"][info.layout],
+                              "layout": LAYOUT_NAMES[info.layout],
                               "consumer_warps": info.consumer_warps},
             "parity": "counts and fitness bit-exact vs reference trace on every batch",
             **({"phases": phases} if phases else {}),

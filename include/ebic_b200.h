@@ -68,7 +68,8 @@ typedef struct ebic_ctx_info {
     int grid;             /* CTAs per count launch on shard 0 */
     size_t device_bytes;  /* matrix bytes resident on shard 0 */
     int sm_count;         /* SMs of shard 0's device */
-    int layout;           /* last count launch: 0 fp64 tile, 1/2 = exact rank tile (planes) */
+    int layout;           /* last count launch: 0 fp64 tile, 1/2 = exact rank tile (planes),
+                             3 = one-plane collapsed rank tile (eps > 0) */
     int consumer_warps;   /* count-kernel consumer warps per CTA */
 } ebic_ctx_info;
 

@@ -122,7 +122,12 @@ struct RankLayout {
     bool ok = false;
     uint64_t eps_bits = 0;
     int planes = 0;
+    bool collapsed = false;            // one plane tested with <= (eps > 0)
     uint16_t* d = nullptr;
+    // rows the collapsed layout cannot represent (evaluated exactly in fp64)
+    unsigned long long* d_row_excl = nullptr;  // bitmask, ceil(ld / 64) words
+    uint32_t* d_excl_rows = nullptr;
+    uint32_t n_excl = 0;
     CUtensorMap tmap;
     bool tmap_ok = false;
     int tmap_slice = 0;
@@ -162,6 +167,7 @@ struct Shard {
     int has_nan = -1;  // -1 unknown
     int last_grid = 0;
     int last_reduce = -1;  // reduction-tail mode of the last launch
+    bool last_collapsed = false;
     CountConfig last_cfg;
 };
 
@@ -455,6 +461,24 @@ uint64_t eps_key(double eps) {
 
 // The exact rank layout of this shard for `eps` (built on first use, two
 // epsilons cached), or nullptr when the fp64 tile must be used.
+template <int PLANES, bool COLLAPSED>
+void launch_rank_build(Shard& s, size_t n_cols, double eps, uint16_t* out, uint8_t* dirty) {
+    uint32_t Kp = 1;
+    while (Kp < PLANES * n_cols) Kp <<= 1;
+    const size_t smem = size_t(Kp) * 16 + 32 * 4 + 64;
+    auto k = rank_build_kernel<PLANES, COLLAPSED>;
+    CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k<<<(unsigned)s.ld, 256, smem, s.stream>>>(s.d_mat, (uint32_t)s.ld, (uint32_t)s.rows,
+                                                (uint32_t)n_cols, eps, Kp, out, dirty);
+    CK(cudaGetLastError());
+}
+
+// The exact rank layout of this shard for `eps` (built on first use, two
+// epsilons cached), or nullptr when the fp64 tile must be used:
+//   eps == 0, no NaN        one plane, strict test        (2 B/cell)
+//   eps > 0, few dirty rows one plane, <= test (collapsed) (2 B/cell) + the
+//                           dirty rows evaluated exactly in fp64 by the kernel
+//   otherwise               two planes (lo, hi)            (4 B/cell)
 RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
     if (n_cols > kRankMaxCols || env_int("EBIC_LAYOUT_F64", 0)) return nullptr;
     const uint64_t key = eps_key(eps);
@@ -476,27 +500,55 @@ RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
         s.has_nan = h;
     }
     RankLayout& rl = s.ranks[0].last_use <= s.ranks[1].last_use ? s.ranks[0] : s.ranks[1];
-    const int planes = (eps == 0.0 && !s.has_nan) ? 1 : 2;
-    if (rl.d && rl.planes != planes) {
-        CK(cudaFree(rl.d));
-        rl.d = nullptr;
-    }
-    if (!rl.d) CK(cudaMalloc(&rl.d, size_t(planes) * s.ld * n_cols * sizeof(uint16_t)));
+    if (!rl.d) CK(cudaMalloc(&rl.d, 2 * s.ld * n_cols * sizeof(uint16_t)));  // room for 2 planes
+    cudaFree(rl.d_row_excl);
+    cudaFree(rl.d_excl_rows);
+    rl.d_row_excl = nullptr;
+    rl.d_excl_rows = nullptr;
+    rl.n_excl = 0;
     rl.ok = false;
     rl.tmap_ok = false;
-    rl.planes = planes;
     rl.eps_bits = key;
-    uint32_t Kp = 1;
-    while (Kp < planes * n_cols) Kp <<= 1;
-    const size_t smem = size_t(Kp) * 16 + 32 * 4 + 64;
-    if (planes == 2) {
-        CK(cudaFuncSetAttribute(rank_build_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        rank_build_kernel<2><<<(unsigned)s.ld, 256, smem, s.stream>>>(s.d_mat, (uint32_t)s.ld, (uint32_t)s.rows, (uint32_t)n_cols, eps, Kp, rl.d);
-    } else {
-        CK(cudaFuncSetAttribute(rank_build_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        rank_build_kernel<1><<<(unsigned)s.ld, 256, smem, s.stream>>>(s.d_mat, (uint32_t)s.ld, (uint32_t)s.rows, (uint32_t)n_cols, eps, Kp, rl.d);
+    rl.collapsed = false;
+    bool done = false;
+    if (eps == 0.0 && !s.has_nan) {
+        rl.planes = 1;
+        launch_rank_build<1, false>(s, n_cols, eps, rl.d, nullptr);
+        done = true;
+    } else if (eps > 0.0 && eps < INFINITY && !env_int("EBIC_NO_COLLAPSE", 0)) {
+        uint8_t* d_dirty = nullptr;
+        CK(cudaMalloc(&d_dirty, s.ld));
+        launch_rank_build<1, true>(s, n_cols, eps, rl.d, d_dirty);
+        std::vector<uint8_t> dirty(s.rows);
+        CK(cudaMemcpyAsync(dirty.data(), d_dirty, s.rows, cudaMemcpyDeviceToHost, s.stream));
+        CK(cudaStreamSynchronize(s.stream));
+        CK(cudaFree(d_dirty));
+        std::vector<uint32_t> rows;
+        for (size_t r = 0; r < s.rows; ++r)
+            if (dirty[r]) rows.push_back((uint32_t)r);
+        // Exact fix-up costs ~P * len fp64 loads per dirty row: worth it while
+        // dirty rows are rare.
+        const size_t limit = std::max<size_t>(64, s.rows / 512);
+        if (rows.size() <= limit) {
+            rl.planes = 1;
+            rl.collapsed = true;
+            rl.n_excl = (uint32_t)rows.size();
+            if (!rows.empty()) {
+                const size_t words = (s.ld + 63) / 64;
+                std::vector<unsigned long long> mask(words, 0ull);
+                for (uint32_t r : rows) mask[r / 64] |= 1ull << (r % 64);
+                CK(cudaMalloc(&rl.d_row_excl, words * 8));
+                CK(cudaMalloc(&rl.d_excl_rows, rows.size() * 4));
+                CK(cudaMemcpy(rl.d_row_excl, mask.data(), words * 8, cudaMemcpyHostToDevice));
+                CK(cudaMemcpy(rl.d_excl_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice));
+            }
+            done = true;
+        }
     }
-    CK(cudaGetLastError());
+    if (!done) {
+        rl.planes = 2;
+        launch_rank_build<2, false>(s, n_cols, eps, rl.d, nullptr);
+    }
     CK(cudaStreamSynchronize(s.stream));
     rl.ok = true;
     rl.last_use = ++s.rank_clock;
@@ -597,8 +649,17 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         if (g_env > 0) grid = std::min<int>(g_env, (int)p.n_tiles);
         s.last_grid = grid;
         s.last_cfg = c;
+        s.last_collapsed = c.layout && rl->collapsed;
         ensure_partial(s, P, grid, p.reduce_striped != 0);
         p.partial = s.d_partial;
+        if (c.layout && rl->collapsed) {
+            p.rank_k = 0x80008000u;
+            p.row_excl = rl->d_row_excl;
+            p.excl_rows = rl->d_excl_rows;
+            p.n_excl = rl->n_excl;
+        } else {
+            p.rank_k = 0x7fff7fffu;
+        }
         const CUtensorMap& tm = c.layout ? rank_tensor_map(*rl, s, ctx.n_cols, c) : tensor_map(s, ctx.n_cols, c);
         launch_tma(c, e0, tm, p, grid, smem, st);
     } else {
@@ -607,6 +668,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         const int grid = (int)((s.rows + 255) / 256);
         s.last_grid = grid;
         s.last_cfg = c;
+        s.last_collapsed = false;
         ensure_partial(s, P, grid, p.reduce_striped != 0);
         p.partial = s.d_partial;
         if (e0) {
@@ -779,7 +841,11 @@ void free_shard(Shard& s) {
     if (s.h_map) cudaFreeHost(s.h_map);
     cudaFree(s.tables.d_log);
     cudaFree(s.tables.d_exp);
-    for (RankLayout& rl : s.ranks) cudaFree(rl.d);
+    for (RankLayout& rl : s.ranks) {
+        cudaFree(rl.d);
+        cudaFree(rl.d_row_excl);
+        cudaFree(rl.d_excl_rows);
+    }
     cudaFree(s.d_phase);
     if (s.stream) cudaStreamDestroy(s.stream);
 }
@@ -914,6 +980,7 @@ int ebic_ctx_get_info(const ebic_ctx* ctx, ebic_ctx_info* info) {
         info->device_bytes = s.ld * ctx->n_cols * sizeof(double);
         info->sm_count = s.sm_count;
         info->layout = s.last_cfg.layout;
+        if (s.last_cfg.layout == 1 && s.last_collapsed) info->layout = 3;
         info->consumer_warps = s.last_cfg.ncw == 32 ? 31 : s.last_cfg.ncw;
     });
 }

@@ -161,6 +161,10 @@ struct CountParams {
     uint32_t max_parts;                    // tail split of the last wave (1 = off)
     uint32_t reduce_striped;               // 1: striped-accumulator tail, 0: reduction tree
     uint32_t scratch_in_stage;             // prologue scratch lives in the last stage buffer
+    uint32_t rank_k;                       // one-plane rank test constant (RankWalker::step)
+    const unsigned long long* __restrict__ row_excl;  // [ceil(rows/64)] rows not in the layout
+    const uint32_t* __restrict__ excl_rows;           // their indices (n_excl)
+    uint32_t n_excl;
     // Optional completion signal for host callers: after the final CTA has
     // written counts/fitness (which may live in mapped host memory), it makes
     // them system-visible and stores done_seq to *done_flag.
@@ -572,11 +576,13 @@ struct F64Walker {
     static constexpr int kColBytes = RPG * 8;      // one column of a staged tile
     static constexpr int kDim0PerTile = RPG;       // TMA dim-0 extent of a tile (fp64 elements)
     using Mask = uint32_t;
-    __device__ __forceinline__ static Mask valid(uint32_t row0, uint32_t n_rows) {
+    // excl: bit k set = the lane's row k is excluded (fixed up separately).
+    __device__ __forceinline__ static Mask valid(uint32_t row0, uint32_t n_rows, uint32_t excl,
+                                                 uint32_t) {
         uint32_t m = 0;
 #pragma unroll
         for (int k = 0; k < RPL; ++k) m |= (row0 + k < n_rows) ? (1u << k) : 0u;
-        return m;
+        return m & ~excl;
     }
 
     static constexpr int kSeriesPerGroup = 1;
@@ -713,13 +719,17 @@ struct RankWalker {
     static constexpr int kSeriesPerGroup = 2;                 // two independent walks per group
     struct Mask {
         uint32_t m[kWords];
+        uint32_t k;  // per-pair constant: 0x7fff7fff (strict <) or 0x80008000 (<=, collapsed)
     };
-    __device__ __forceinline__ static Mask valid(uint32_t row0, uint32_t n_rows) {
+    // excl: bit j set = the lane's row j is excluded (fixed up separately).
+    __device__ __forceinline__ static Mask valid(uint32_t row0, uint32_t n_rows, uint32_t excl,
+                                                 uint32_t kconst) {
         Mask v;
 #pragma unroll
         for (int k = 0; k < kWords; ++k)
-            v.m[k] = ((row0 + 2 * k < n_rows) ? 0x8000u : 0u) |
-                     ((row0 + 2 * k + 1 < n_rows) ? 0x80000000u : 0u);
+            v.m[k] = ((row0 + 2 * k < n_rows && !((excl >> (2 * k)) & 1u)) ? 0x8000u : 0u) |
+                     ((row0 + 2 * k + 1 < n_rows && !((excl >> (2 * k + 1)) & 1u)) ? 0x80000000u : 0u);
+        v.k = PLANES == 2 ? 0x7fff7fffu : kconst;
         return v;
     }
     // 32-bit shared-window address arithmetic: one add per element.
@@ -743,16 +753,19 @@ struct RankWalker {
             }
         }
     }
-    // One adjacent pair: ok[k] accumulates bit 15/31 per row.
-    __device__ __forceinline__ static void step(uint32_t* ok, const uint4& prev, const uint4& cur) {
+    // One adjacent pair: ok[k] accumulates bit 15/31 per row.  With one
+    // plane, K = 0x7fff7fff tests r(prev) < r(cur) (eps == 0) and
+    // K = 0x80008000 tests r(prev) <= r(cur) (collapsed eps > 0 layout).
+    __device__ __forceinline__ static void step(uint32_t* ok, const uint4& prev, const uint4& cur,
+                                                uint32_t K) {
         if (PLANES == 2) {
             ok[0] &= cur.z - prev.x + 0x7fff7fffu;
             ok[1] &= cur.w - prev.y + 0x7fff7fffu;
         } else {
-            ok[0] &= cur.x - prev.x + 0x7fff7fffu;
-            ok[1] &= cur.y - prev.y + 0x7fff7fffu;
-            ok[2] &= cur.z - prev.z + 0x7fff7fffu;
-            ok[3] &= cur.w - prev.w + 0x7fff7fffu;
+            ok[0] &= cur.x - prev.x + K;
+            ok[1] &= cur.y - prev.y + K;
+            ok[2] &= cur.z - prev.z + K;
+            ok[3] &= cur.w - prev.w + K;
         }
     }
     __device__ __forceinline__ static uint32_t tally(const uint32_t* ok, const Mask& vm) {
@@ -776,8 +789,8 @@ struct RankWalker {
         for (int i = 1; i < L; ++i) {
             const uint4 cura = ld(base, wa[i]);
             const uint4 curb = ld(base, wb[i]);
-            step(oka, preva, cura);
-            step(okb, prevb, curb);
+            step(oka, preva, cura, vm.k);
+            step(okb, prevb, curb, vm.k);
             preva = cura;
             prevb = curb;
         }
@@ -792,7 +805,7 @@ struct RankWalker {
             uint4 prev = ld(base, pc[0]);
             for (uint32_t i = 1; i < len; ++i) {
                 const uint4 cur = ld(base, pc[i]);
-                step(ok, prev, cur);
+                step(ok, prev, cur, vm.k);
                 prev = cur;
             }
         }
@@ -958,8 +971,16 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             }
             mbar_wait(&full_bar[st], phase);
             const unsigned char* base = stage_base + size_t(st) * p.stage_bytes + gl * Walker::kLaneBytes;
-            // rows of this tile that exist (the last tile may be partial)
-            const typename Walker::Mask vmask = Walker::valid(tile * RPG + gl * RPL, p.n_rows);
+            // rows of this tile that exist (the last tile may be partial), minus
+            // rows the layout cannot represent (fixed up below)
+            uint32_t excl = 0;
+            if (p.row_excl) {
+                const uint32_t r0 = tile * RPG + gl * RPL;
+                excl = static_cast<uint32_t>(__ldg(p.row_excl + (r0 >> 6)) >> (r0 & 63)) &
+                       ((1u << RPL) - 1u);
+            }
+            const typename Walker::Mask vmask =
+                Walker::valid(tile * RPG + gl * RPL, p.n_rows, excl, p.rank_k);
 
             // Chunks are handed out dynamically (longest first: slots are
             // sorted by ascending length) so the warps of the CTA finish a
@@ -1003,6 +1024,46 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);
             if (++st == p.stages) st = 0, phase ^= 1u;
+        }
+        // Rows excluded from the layout (collapsed rank layout: rows with values
+        // closer than eps, or NaN) are evaluated exactly on the fp64 matrix,
+        // one row per CTA in turn: the row is gathered into the (now idle)
+        // first stage buffer with one round of independent loads, then every
+        // thread walks one series from shared memory.
+        // Dirty rows go to the last CTAs first: those carry no tail-split item.
+        const uint32_t rb = G - 1 - blockIdx.x;
+        if (rb < p.n_excl) {
+            const uint32_t nt = NCW * 32;
+            double* rowbuf = reinterpret_cast<double*>(stage_base);
+            const bool fits = size_t(p.n_cols) * sizeof(double) <= size_t(p.stages) * p.stage_bytes;
+            named_bar_sync(1, nt);  // every consumer is done with the stage buffers
+            for (uint32_t i = rb; i < p.n_excl; i += G) {
+                const uint32_t row = __ldg(p.excl_rows + i);
+                const double* col0 = p.matrix + row;
+                if (fits)
+                    for (uint32_t c = threadIdx.x; c < p.n_cols; c += nt)
+                        rowbuf[c] = __ldg(col0 + size_t(c) * p.ld);
+                named_bar_sync(1, nt);
+                for (uint32_t g = threadIdx.x; g < P; g += nt) {
+                    const uint32_t len = wl.slen[g];
+                    const uint32_t* pc = wl.pcols + wl.sstart[g];
+                    auto value = [&](uint32_t k) {
+                        const uint32_t c = pc[k] / Walker::kColBytes;
+                        return fits ? rowbuf[c] : __ldg(col0 + size_t(c) * p.ld);
+                    };
+                    bool ok = true;
+                    if (len > 1) {
+                        double prev = value(0);
+                        for (uint32_t k = 1; k < len; ++k) {
+                            const double cur = value(k);
+                            ok = ok & step_ok<false>(prev, cur, eps);
+                            prev = cur;
+                        }
+                    }
+                    if (ok) atomicAdd(&wl.cnt[g], 1u);
+                }
+                named_bar_sync(1, nt);
+            }
         }
     }
     __syncthreads();
@@ -1067,10 +1128,21 @@ __device__ __forceinline__ uint64_t sortable_key(double x) {
     return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
-template <int PLANES>
+__device__ __forceinline__ double key_value(uint64_t k) {
+    const uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double(static_cast<long long>(u));
+}
+
+// PLANES == 1 && COLLAPSED (eps > 0): one plane of dense value ranks tested
+// with <= ; valid for a row iff every distinct value s has fl(s + eps) > s and
+// the next larger distinct value exceeds fl(s + eps) (then, for all a, b:
+// v_a < fl(v_b + eps) <=> v_a <= v_b).  Rows failing that (or holding NaN)
+// are flagged in dirty_out and evaluated exactly on the fp64 matrix.
+template <int PLANES, bool COLLAPSED = false>
 __global__ void __launch_bounds__(256)
     rank_build_kernel(const double* __restrict__ mat, uint32_t ld, uint32_t n_rows,
-                      uint32_t n_cols, double eps, uint32_t Kp, uint16_t* __restrict__ out) {
+                      uint32_t n_cols, double eps, uint32_t Kp, uint16_t* __restrict__ out,
+                      uint8_t* __restrict__ dirty_out = nullptr) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* key = reinterpret_cast<uint64_t*>(smem);
     uint32_t* pay = reinterpret_cast<uint32_t*>(key + Kp);
@@ -1094,6 +1166,8 @@ __global__ void __launch_bounds__(256)
         return;
     }
     const uint32_t K = PLANES * n_cols;
+    __shared__ int s_dirty;
+    if (tid == 0) s_dirty = 0;
     for (uint32_t i = tid; i < Kp; i += nt) {
         uint64_t k = ~0ull;
         uint32_t pl = 0xffffffffu;
@@ -1130,6 +1204,21 @@ __global__ void __launch_bounds__(256)
     auto is_new = [&](uint32_t i) -> uint32_t {
         return key[i] != ~0ull && (i == 0 || key[i] != key[i - 1]) ? 1u : 0u;
     };
+    if (COLLAPSED) {
+        for (uint32_t i = tid; i < K; i += nt) {
+            if (key[i] == ~0ull) {  // NaN cell
+                s_dirty = 1;
+                continue;
+            }
+            const double x = key_value(key[i]);
+            const double t = __dadd_rn(x, eps);
+            bool bad = !(t > x);
+            if (i + 1 < K && key[i + 1] != ~0ull && key[i + 1] != key[i])
+                bad = bad || !(key_value(key[i + 1]) > t);
+            if (bad) s_dirty = 1;
+        }
+        __syncthreads();
+    }
     block_exclusive_scan(Kp, is_new, rk, wsum, tid, nt, 0);
     __syncthreads();
     for (uint32_t i = tid; i < Kp; i += nt) {
@@ -1141,6 +1230,7 @@ __global__ void __launch_bounds__(256)
         else v = static_cast<uint16_t>((rk[i] + is_new(i)) | 0x8000u);
         out[at(c, plane)] = v;
     }
+    if (COLLAPSED && tid == 0) dirty_out[r] = static_cast<uint8_t>(s_dirty);
 }
 
 // Sets *flag if any real (non-padding) cell of the column-major matrix is NaN.

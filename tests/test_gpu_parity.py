@@ -22,7 +22,7 @@ port = oracle.Port()
 # Every count-kernel configuration the library can select: the exact rank
 # tile (default; 1 or 2 planes by eps / NaN presence, 16 or 31 consumer warps),
 # the fp64 tile (rows-per-tile x rows-per-lane), and the unstaged direct kernel.
-KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16")] +
+KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NO_COLLAPSE="1")] +
                   [dict(EBIC_LAYOUT_F64="1", EBIC_RPG=str(g), EBIC_RPL=str(l))
                    for g in (32, 16, 8, 4) for l in (1, 2)] +
                   [dict(EBIC_LAYOUT_F64="1", EBIC_NCW="16"), dict(EBIC_FORCE_DIRECT="1")])
@@ -112,7 +112,7 @@ def test_every_kernel_config_on_traces(cfg, name):
                 assert bits_equal(f, fit)
 
 
-@pytest.mark.parametrize("cfg", KERNEL_CONFIGS[:3] + KERNEL_CONFIGS[5:6] + KERNEL_CONFIGS[-1:], ids=str)
+@pytest.mark.parametrize("cfg", KERNEL_CONFIGS[:4] + KERNEL_CONFIGS[6:7] + KERNEL_CONFIGS[-1:], ids=str)
 def test_edge_cases_vs_oracle(cfg):
     """Ragged row counts, ties, +-0, NaN/inf cells, odd eps values, len-1 series."""
     rng = np.random.default_rng(7)
@@ -282,3 +282,32 @@ def test_finalize_biclusters_c4_top_series():
         core = port.assign_rows(v, b.series, t.eps)
         wr, wf = port.expand_bicluster(v, b.series, core, [0] * len(core), True, 1, t.eps)
         assert b.rows == wr and [int(f) for f in b.row_flags] == wf
+
+
+@pytest.mark.parametrize("n_dirty", [0, 1, 7, 40, 3000])
+def test_collapsed_rank_layout_with_dirty_rows(n_dirty):
+    """eps > 0 with clean rows uses the one-plane collapsed layout (<= test);
+    rows holding two values closer than eps (or NaN) cannot be represented and
+    are evaluated exactly in fp64 by the kernel.  Too many of them: two planes."""
+    rng = np.random.default_rng(100 + n_dirty)
+    rows, n_cols, eps = 6000, 60, 1e-6
+    v = rng.standard_normal((rows, n_cols))
+    dirty = rng.choice(rows, size=n_dirty, replace=False)
+    for k, r in enumerate(dirty):
+        a, b = rng.choice(n_cols, size=2, replace=False)
+        if k % 5 == 4:
+            v[r, a] = np.nan
+        else:
+            v[r, b] = v[r, a] + eps * [0.5, 1.0, 0.999, 0.25][k % 4]  # inside (v_a, v_a + eps]
+    series = random_population(rng, n_cols, 700)
+    pop = cbf(series)
+    with eb.Evaluator(v) as ev:
+        for e in (eps, 2 * eps, 1e-9):
+            got = ev.count_matches(pop, e)
+            want = port.count_matches(v, pop.offsets, pop.col_indices, e)
+            assert (got == want).all(), (n_dirty, e)
+            f = ev.evaluate_population(pop, eb.FitnessParams(120), e)
+            _, wf = port.evaluate_population(v, pop.offsets, pop.col_indices, 120, e)
+            assert bits_equal(f, wf)
+        info = ev.info()
+    assert info.layout == (3 if n_dirty <= 64 else 2)
