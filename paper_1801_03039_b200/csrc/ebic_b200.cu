@@ -67,6 +67,31 @@ int env_int(const char* name, int dflt) {
     return (v && *v) ? std::atoi(v) : dflt;
 }
 
+// Tuning / test overrides (EBIC_* environment variables), read once when a
+// context is created so the per-generation launch path makes no getenv calls.
+struct Knobs {
+    int force_direct, rpg, rpl, stages, ncw, slice, layout_f64, no_collapse, sched_static,
+        max_parts, reduce_tree, grid, phase_timing, spg;
+    static Knobs from_env() {
+        Knobs k;
+        k.force_direct = env_int("EBIC_FORCE_DIRECT", 0);
+        k.rpg = env_int("EBIC_RPG", 0);
+        k.rpl = env_int("EBIC_RPL", 0);
+        k.stages = env_int("EBIC_STAGES", 0);
+        k.ncw = env_int("EBIC_NCW", 0);
+        k.slice = env_int("EBIC_SLICE", 0);
+        k.layout_f64 = env_int("EBIC_LAYOUT_F64", 0);
+        k.no_collapse = env_int("EBIC_NO_COLLAPSE", 0);
+        k.sched_static = env_int("EBIC_SCHED_STATIC", 0);
+        k.max_parts = env_int("EBIC_MAX_PARTS", 8);
+        k.reduce_tree = env_int("EBIC_REDUCE_TREE", 0);
+        k.grid = env_int("EBIC_GRID", 0);
+        k.phase_timing = env_int("EBIC_PHASE_TIMING", 0);
+        k.spg = env_int("EBIC_SPG", 0);
+        return k;
+    }
+};
+
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -106,6 +131,7 @@ struct CountConfig {
     int rpl = 1;        // rows per lane
     int ncw = 16;       // consumer warps per CTA
     int slice = 0;      // rank layout: bytes per staged column slice (64 or 128)
+    int spg = 2;        // rank layout: series per lane group
     int stages = 0;
     uint32_t box_cols = 0, n_boxes = 0, stage_bytes = 0;
 };
@@ -136,6 +162,7 @@ struct RankLayout {
 
 struct Shard {
     int device = 0;
+    Knobs knobs = Knobs::from_env();
     size_t row_begin = 0;  // global first row
     size_t rows = 0;
     size_t ld = 0;         // padded leading dimension (multiple of 64)
@@ -168,6 +195,10 @@ struct Shard {
     int last_grid = 0;
     int last_reduce = -1;  // reduction-tail mode of the last launch
     bool last_collapsed = false;
+    // choose_config memo (same P / L / layout as the previous launch)
+    size_t memo_P = 0, memo_L = 0;
+    int memo_planes = -1;
+    CountConfig memo_cfg;
     CountConfig last_cfg;
 };
 
@@ -251,7 +282,7 @@ void upload_shard(Shard& s, const double* src_rows, size_t n_cols, bool src_on_d
     s.ld = std::max<size_t>(64, (s.rows + 63) / 64 * 64);
     CK(cudaMalloc(&s.d_mat, s.ld * n_cols * sizeof(double)));
     CK(cudaMalloc(&s.d_done, (kMaxGroups + 1) * sizeof(unsigned int)));
-    if (env_int("EBIC_PHASE_TIMING", 0)) {
+    if (s.knobs.phase_timing) {
         CK(cudaMalloc(&s.d_phase, 4096 * 8 * sizeof(unsigned long long)));
         CK(cudaMemsetAsync(s.d_phase, 0, 4096 * 8 * sizeof(unsigned long long), s.stream));
     }
@@ -349,14 +380,15 @@ bool fit_ring(CountConfig& c, size_t n_cols, size_t col_bytes, size_t P, size_t 
 // rows) that leaves a >= 3-deep TMA ring; else the unstaged direct kernel.
 CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int rank_planes) {
     CountConfig best;
-    if (env_int("EBIC_FORCE_DIRECT", 0)) return best;
-    const int want_rpg = env_int("EBIC_RPG", 0);
-    const int want_rpl = env_int("EBIC_RPL", 0);
-    const int want_stages = env_int("EBIC_STAGES", 0);
-    const int want_ncw = env_int("EBIC_NCW", 0);
+    const Knobs& kn = s.knobs;
+    if (kn.force_direct) return best;
+    const int want_rpg = kn.rpg;
+    const int want_rpl = kn.rpl;
+    const int want_stages = kn.stages;
+    const int want_ncw = kn.ncw;
     const size_t budget = (size_t)s.max_smem;
     if (rank_planes) {
-        const int want_slice = env_int("EBIC_SLICE", 0);
+        const int want_slice = kn.slice;
         for (int min_stages : {3, 2}) {
             for (int slice : {128, 64}) {
                 if (want_slice && slice != want_slice) continue;
@@ -365,7 +397,12 @@ CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int
                 c.slice = slice;
                 c.rpg = slice / (2 * rank_planes);
                 c.rpl = rank_planes == 2 ? 4 : 8;
-                c.ncw = want_ncw == 16 ? 16 : 32;
+                // one plane: 16 warps (92 registers, no spills) measured faster than
+                // 31 warps (64-register cap spills the 4 ok-words x 2 walks);
+                // two planes: 31 warps.
+                c.ncw = want_ncw ? (want_ncw == 16 ? 16 : 32) : (rank_planes == 1 ? 16 : 32);
+                c.spg = kn.spg == 4 ? 4 : 2;
+                if (c.spg == 4) c.ncw = 16;  // 4 walks per group need the 16-warp register budget
                 if (fit_ring(c, n_cols, slice, P, L, budget, min_stages, want_stages)) return c;
             }
         }
@@ -412,6 +449,17 @@ void launch_tma(const CountConfig& c, bool e0, const CUtensorMap& tm, const Coun
                 int grid, size_t smem, cudaStream_t st) {
     if (c.layout) {
         const bool n16 = c.ncw == 16, s64 = c.slice == 64;
+        if (c.spg == 4) {
+            if (c.layout == 2) {
+                if (s64) launch_tma_t<RankWalker<2, 64, 4>, 16>(tm, p, grid, smem, st);
+                else launch_tma_t<RankWalker<2, 128, 4>, 16>(tm, p, grid, smem, st);
+            } else {
+                if (s64) launch_tma_t<RankWalker<1, 64, 4>, 16>(tm, p, grid, smem, st);
+                else launch_tma_t<RankWalker<1, 128, 4>, 16>(tm, p, grid, smem, st);
+            }
+            CK(cudaGetLastError());
+            return;
+        }
         if (c.layout == 2) {
             if (s64) {
                 if (n16) launch_tma_t<RankWalker<2, 64>, 16>(tm, p, grid, smem, st);
@@ -480,7 +528,7 @@ void launch_rank_build(Shard& s, size_t n_cols, double eps, uint16_t* out, uint8
 //                           dirty rows evaluated exactly in fp64 by the kernel
 //   otherwise               two planes (lo, hi)            (4 B/cell)
 RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
-    if (n_cols > kRankMaxCols || env_int("EBIC_LAYOUT_F64", 0)) return nullptr;
+    if (n_cols > kRankMaxCols || s.knobs.layout_f64) return nullptr;
     const uint64_t key = eps_key(eps);
     for (RankLayout& rl : s.ranks)
         if (rl.ok && rl.eps_bits == key) {
@@ -515,7 +563,7 @@ RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
         rl.planes = 1;
         launch_rank_build<1, false>(s, n_cols, eps, rl.d, nullptr);
         done = true;
-    } else if (eps > 0.0 && eps < INFINITY && !env_int("EBIC_NO_COLLAPSE", 0)) {
+    } else if (eps > 0.0 && eps < INFINITY && !s.knobs.no_collapse) {
         uint8_t* d_dirty = nullptr;
         CK(cudaMalloc(&d_dirty, s.ld));
         launch_rank_build<1, true>(s, n_cols, eps, rl.d, d_dirty);
@@ -621,9 +669,9 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
     p.matrix = s.d_mat;
     p.ld = (uint32_t)s.ld;
     p.cols_base = cols_base;
-    p.sched_static = (uint32_t)env_int("EBIC_SCHED_STATIC", 0);
-    p.max_parts = (uint32_t)env_int("EBIC_MAX_PARTS", 8);
-    p.reduce_striped = env_int("EBIC_REDUCE_TREE", 0) ? 0u : 1u;
+    p.sched_static = (uint32_t)s.knobs.sched_static;
+    p.max_parts = (uint32_t)s.knobs.max_parts;
+    p.reduce_striped = s.knobs.reduce_tree ? 0u : 1u;
     p.done_flag = done_flag;
     p.done_seq = done_seq;
     p.phase_ns = s.d_phase;
@@ -635,7 +683,12 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
     }
     const bool e0 = (eps == 0.0);
     RankLayout* rl = ensure_ranks(s, ctx.n_cols, eps);
-    CountConfig c = choose_config(s, ctx.n_cols, P, L, rl ? rl->planes : 0);
+    const int planes = rl ? rl->planes : 0;
+    if (!(s.memo_P == P && s.memo_L == L && s.memo_planes == planes)) {
+        s.memo_cfg = choose_config(s, ctx.n_cols, P, L, planes);
+        s.memo_P = P, s.memo_L = L, s.memo_planes = planes;
+    }
+    const CountConfig c = s.memo_cfg;
     if (c.rpg) {
         p.box_cols = c.box_cols;
         p.n_boxes = c.n_boxes;
@@ -645,7 +698,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         p.scratch_in_stage = scratch_in_stage(c, P, L) ? 1u : 0u;
         const size_t smem = tma_smem_bytes(c, P, L);
         int grid = std::min<int>((int)p.n_tiles, s.sm_count);
-        const int g_env = env_int("EBIC_GRID", 0);
+        const int g_env = s.knobs.grid;
         if (g_env > 0) grid = std::min<int>(g_env, (int)p.n_tiles);
         s.last_grid = grid;
         s.last_cfg = c;

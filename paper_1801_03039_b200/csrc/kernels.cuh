@@ -706,7 +706,7 @@ struct F64Walker {
 //     8 rows (one LDS.128).
 // Tile: 128 bytes per column (32 rows x 2 planes, or 64 rows x 1 plane).
 // ---------------------------------------------------------------------------
-template <int PLANES, int SLICE>
+template <int PLANES, int SLICE, int SPG = 2>
 struct RankWalker {
     static_assert(SLICE == 64 || SLICE == 128, "column slice of 64 or 128 bytes");
     static constexpr int kRowsPerLane = PLANES == 2 ? 4 : 8;
@@ -716,7 +716,9 @@ struct RankWalker {
     static constexpr int kShift = SLICE == 128 ? 7 : 6;
     static constexpr int kDim0PerTile = kRowsPerTile * PLANES;  // u16 elements
     static constexpr int kWords = kRowsPerLane / 2;           // ok words per lane
-    static constexpr int kSeriesPerGroup = 2;                 // two independent walks per group
+    static constexpr int kSeriesPerGroup = SPG;               // independent walks per group
+    static constexpr int kFieldBits = 32 / SPG;               // packed per-series counts
+    static_assert(SPG == 2 || SPG == 4, "2 or 4 series per lane group");
     struct Mask {
         uint32_t m[kWords];
         uint32_t k;  // per-pair constant: 0x7fff7fff (strict <) or 0x80008000 (<=, collapsed)
@@ -811,7 +813,38 @@ struct RankWalker {
         }
         return tally(ok, vm);
     }
-    // Counts of slots g0 and g0+1 (16-bit fields).  `uniform`: every slot of
+    // SPG series of exactly L columns, walked interleaved (independent chains).
+    template <int L>
+    __device__ __forceinline__ static uint32_t countN_fixed(uint32_t base, const WorkList& wl,
+                                                            uint32_t g0, const Mask& vm) {
+        uint32_t w[SPG][12];
+#pragma unroll
+        for (int q = 0; q < SPG; ++q) load_offs(w[q], wl.pcols + wl.sstart[g0 + q], L);
+        uint32_t ok[SPG][kWords];
+        uint4 prev[SPG];
+#pragma unroll
+        for (int q = 0; q < SPG; ++q) {
+#pragma unroll
+            for (int k = 0; k < kWords; ++k) ok[q][k] = 0xffffffffu;
+            prev[q] = ld(base, w[q][0]);
+        }
+#pragma unroll
+        for (int i = 1; i < L; ++i) {
+#pragma unroll
+            for (int q = 0; q < SPG; ++q) {
+                const uint4 cur = ld(base, w[q][i]);
+                step(ok[q], prev[q], cur, vm.k);
+                prev[q] = cur;
+            }
+        }
+        uint32_t c = 0;
+#pragma unroll
+        for (int q = 0; q < SPG; ++q) c |= tally(ok[q], vm) << (q * kFieldBits);
+        return c;
+    }
+
+    // Counts of slots g0 .. g0+SPG-1 (packed kFieldBits-bit fields; a group
+    // covers at most 64 rows, so 8 bits suffice).  `uniform`: every slot of
     // the warp's chunk exists and has length ulen.
     __device__ __forceinline__ static uint32_t count_group(const unsigned char* base_ptr,
                                                            const WorkList& wl, uint32_t g0,
@@ -819,26 +852,26 @@ struct RankWalker {
                                                            double, const Mask& vm) {
         const uint32_t base = smem_u32(base_ptr);
         if (uniform) {
-            const uint32_t* pa = wl.pcols + wl.sstart[g0];
-            const uint32_t* pb = wl.pcols + wl.sstart[g0 + 1];
             switch (ulen) {
-                case 2: return count2_fixed<2>(base, pa, pb, vm);
-                case 3: return count2_fixed<3>(base, pa, pb, vm);
-                case 4: return count2_fixed<4>(base, pa, pb, vm);
-                case 5: return count2_fixed<5>(base, pa, pb, vm);
-                case 6: return count2_fixed<6>(base, pa, pb, vm);
-                case 7: return count2_fixed<7>(base, pa, pb, vm);
-                case 8: return count2_fixed<8>(base, pa, pb, vm);
-                case 9: return count2_fixed<9>(base, pa, pb, vm);
-                case 10: return count2_fixed<10>(base, pa, pb, vm);
-                case 11: return count2_fixed<11>(base, pa, pb, vm);
-                case 12: return count2_fixed<12>(base, pa, pb, vm);
+                case 2: return countN_fixed<2>(base, wl, g0, vm);
+                case 3: return countN_fixed<3>(base, wl, g0, vm);
+                case 4: return countN_fixed<4>(base, wl, g0, vm);
+                case 5: return countN_fixed<5>(base, wl, g0, vm);
+                case 6: return countN_fixed<6>(base, wl, g0, vm);
+                case 7: return countN_fixed<7>(base, wl, g0, vm);
+                case 8: return countN_fixed<8>(base, wl, g0, vm);
+                case 9: return countN_fixed<9>(base, wl, g0, vm);
+                case 10: return countN_fixed<10>(base, wl, g0, vm);
+                case 11: return countN_fixed<11>(base, wl, g0, vm);
+                case 12: return countN_fixed<12>(base, wl, g0, vm);
                 default: break;
             }
         }
         uint32_t c = 0;
-        if (g0 < P) c = count_any(base, wl.pcols + wl.sstart[g0], wl.slen[g0], vm);
-        if (g0 + 1 < P) c |= count_any(base, wl.pcols + wl.sstart[g0 + 1], wl.slen[g0 + 1], vm) << 16;
+#pragma unroll
+        for (int q = 0; q < SPG; ++q)
+            if (g0 + q < P)
+                c |= count_any(base, wl.pcols + wl.sstart[g0 + q], wl.slen[g0 + q], vm) << (q * kFieldBits);
         return c;
     }
 };
@@ -1013,9 +1046,11 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
 #pragma unroll
                 for (int o = GL / 2; o >= 1; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
                 if (gl == 0) {
+                    constexpr int kBits = 32 / SPG;
+                    constexpr uint32_t kFieldMask = (kBits == 32) ? 0xffffffffu : ((1u << kBits) - 1u);
 #pragma unroll
                     for (int q = 0; q < SPG; ++q) {
-                        const uint32_t cq = (c >> (16 * q)) & 0xffffu;
+                        const uint32_t cq = (c >> (kBits * q)) & kFieldMask;
                         // warps on different tiles may hold the same chunk
                         if (g0 + q < P && cq) atomicAdd(&wl.cnt[g0 + q], cq);
                     }
