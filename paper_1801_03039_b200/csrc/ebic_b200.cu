@@ -153,6 +153,7 @@ struct RankLayout {
     // rows the collapsed layout cannot represent (evaluated exactly in fp64)
     unsigned long long* d_row_excl = nullptr;  // bitmask, ceil(ld / 64) words
     uint32_t* d_excl_rows = nullptr;
+    double* d_excl_vals = nullptr;             // their values, row-major
     uint32_t n_excl = 0;
     CUtensorMap tmap;
     bool tmap_ok = false;
@@ -551,8 +552,10 @@ RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
     if (!rl.d) CK(cudaMalloc(&rl.d, 2 * s.ld * n_cols * sizeof(uint16_t)));  // room for 2 planes
     cudaFree(rl.d_row_excl);
     cudaFree(rl.d_excl_rows);
+    cudaFree(rl.d_excl_vals);
     rl.d_row_excl = nullptr;
     rl.d_excl_rows = nullptr;
+    rl.d_excl_vals = nullptr;
     rl.n_excl = 0;
     rl.ok = false;
     rl.tmap_ok = false;
@@ -589,6 +592,10 @@ RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
                 CK(cudaMalloc(&rl.d_excl_rows, rows.size() * 4));
                 CK(cudaMemcpy(rl.d_row_excl, mask.data(), words * 8, cudaMemcpyHostToDevice));
                 CK(cudaMemcpy(rl.d_excl_rows, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice));
+                CK(cudaMalloc(&rl.d_excl_vals, rows.size() * n_cols * sizeof(double)));
+                gather_rows_kernel<<<(unsigned)rows.size(), 256, 0, s.stream>>>(
+                    s.d_mat, s.ld, (uint32_t)n_cols, rl.d_excl_rows, rl.d_excl_vals);
+                CK(cudaGetLastError());
             }
             done = true;
         }
@@ -709,6 +716,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
             p.rank_k = 0x80008000u;
             p.row_excl = rl->d_row_excl;
             p.excl_rows = rl->d_excl_rows;
+            p.excl_vals = rl->d_excl_vals;
             p.n_excl = rl->n_excl;
         } else {
             p.rank_k = 0x7fff7fffu;
@@ -898,6 +906,7 @@ void free_shard(Shard& s) {
         cudaFree(rl.d);
         cudaFree(rl.d_row_excl);
         cudaFree(rl.d_excl_rows);
+        cudaFree(rl.d_excl_vals);
     }
     cudaFree(s.d_phase);
     if (s.stream) cudaStreamDestroy(s.stream);

@@ -164,6 +164,7 @@ struct CountParams {
     uint32_t rank_k;                       // one-plane rank test constant (RankWalker::step)
     const unsigned long long* __restrict__ row_excl;  // [ceil(rows/64)] rows not in the layout
     const uint32_t* __restrict__ excl_rows;           // their indices (n_excl)
+    const double* __restrict__ excl_vals;             // their values, row-major [n_excl][n_cols]
     uint32_t n_excl;
     // Optional completion signal for host callers: after the final CTA has
     // written counts/fitness (which may live in mapped host memory), it makes
@@ -814,25 +815,33 @@ struct RankWalker {
         return tally(ok, vm);
     }
     // SPG series of exactly L columns, walked interleaved (independent chains).
+    // Column offsets are fetched 4 at a time (one LDS.128 per series) just
+    // ahead of use, keeping 4 offset registers per series live instead of L.
     template <int L>
     __device__ __forceinline__ static uint32_t countN_fixed(uint32_t base, const WorkList& wl,
                                                             uint32_t g0, const Mask& vm) {
-        uint32_t w[SPG][12];
-#pragma unroll
-        for (int q = 0; q < SPG; ++q) load_offs(w[q], wl.pcols + wl.sstart[g0 + q], L);
+        const uint32_t* pc[SPG];
+        uint4 w[SPG];
         uint32_t ok[SPG][kWords];
         uint4 prev[SPG];
 #pragma unroll
         for (int q = 0; q < SPG; ++q) {
+            pc[q] = wl.pcols + wl.sstart[g0 + q];
+            w[q] = *reinterpret_cast<const uint4*>(pc[q]);
 #pragma unroll
             for (int k = 0; k < kWords; ++k) ok[q][k] = 0xffffffffu;
-            prev[q] = ld(base, w[q][0]);
+            prev[q] = ld(base, w[q].x);
         }
 #pragma unroll
         for (int i = 1; i < L; ++i) {
+            if ((i & 3) == 0) {
+#pragma unroll
+                for (int q = 0; q < SPG; ++q) w[q] = *reinterpret_cast<const uint4*>(pc[q] + i);
+            }
 #pragma unroll
             for (int q = 0; q < SPG; ++q) {
-                const uint4 cur = ld(base, w[q][i]);
+                const uint32_t off = (i & 3) == 0 ? w[q].x : (i & 3) == 1 ? w[q].y : (i & 3) == 2 ? w[q].z : w[q].w;
+                const uint4 cur = ld(base, off);
                 step(ok[q], prev[q], cur, vm.k);
                 prev[q] = cur;
             }
@@ -989,9 +998,34 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         if (threadIdx.x == 0) mbar_arrive(prol_bar);
         if (stamp && threadIdx.x == 0) stamp[1] = global_ns();
 
+        // Rows excluded from the layout (collapsed rank layout: two values
+        // closer than eps, or NaN) are evaluated exactly in fp64 before the
+        // first tile, while its TMA load is still in flight: one row per CTA
+        // in turn (the last CTAs first: they carry no tail-split item), one
+        // series per thread, reading a contiguous row copy (gathered once per
+        // context) through L1.
+        for (uint32_t i = G - 1 - blockIdx.x; i < p.n_excl; i += G) {
+            const double* rowv = p.excl_vals + size_t(i) * p.n_cols;
+            for (uint32_t g = threadIdx.x; g < P; g += NCW * 32) {
+                const uint32_t len = wl.slen[g];
+                const uint32_t* pc = wl.pcols + wl.sstart[g];
+                bool ok = true;
+                if (len > 1) {
+                    double prev = __ldg(rowv + pc[0] / Walker::kColBytes);
+                    for (uint32_t k = 1; k < len; ++k) {
+                        const double cur = __ldg(rowv + pc[k] / Walker::kColBytes);
+                        ok = ok & step_ok<false>(prev, cur, p.eps);
+                        prev = cur;
+                    }
+                }
+                if (ok) atomicAdd(&wl.cnt[g], 1u);
+            }
+        }
+
         const int grp = lane / GL;   // group within warp
         const int gl = lane % GL;    // lane within group
         const double eps = p.eps;
+        const bool sched_static = p.sched_static != 0;
 
         uint32_t st = 0, phase = 0;
         for (uint32_t item = blockIdx.x; item < n_items; item += G) {
@@ -1002,18 +1036,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                 c_lo = part * n_chunks / parts;
                 c_hi = (part + 1) * n_chunks / parts;
             }
+            // rows the layout cannot represent (fixed up below): the mask word is
+            // fetched before the stage wait so its latency hides behind it
+            uint32_t excl = 0;
+            const uint32_t r0 = tile * RPG + gl * RPL;
+            unsigned long long excl_word = 0ull;
+            if (p.row_excl) excl_word = __ldg(p.row_excl + (r0 >> 6));
             mbar_wait(&full_bar[st], phase);
             const unsigned char* base = stage_base + size_t(st) * p.stage_bytes + gl * Walker::kLaneBytes;
-            // rows of this tile that exist (the last tile may be partial), minus
-            // rows the layout cannot represent (fixed up below)
-            uint32_t excl = 0;
-            if (p.row_excl) {
-                const uint32_t r0 = tile * RPG + gl * RPL;
-                excl = static_cast<uint32_t>(__ldg(p.row_excl + (r0 >> 6)) >> (r0 & 63)) &
-                       ((1u << RPL) - 1u);
-            }
-            const typename Walker::Mask vmask =
-                Walker::valid(tile * RPG + gl * RPL, p.n_rows, excl, p.rank_k);
+            if (p.row_excl) excl = static_cast<uint32_t>(excl_word >> (r0 & 63)) & ((1u << RPL) - 1u);
+            // rows of this tile that exist (the last tile may be partial)
+            const typename Walker::Mask vmask = Walker::valid(r0, p.n_rows, excl, p.rank_k);
 
             // Chunks are handed out dynamically (longest first: slots are
             // sorted by ascending length) so the warps of the CTA finish a
@@ -1022,7 +1055,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             const uint32_t n_here = c_hi - c_lo;
             uint32_t stat_k = warp;
             auto grab = [&]() {
-                if (p.sched_static) {
+                if (sched_static) {
                     const uint32_t v = stat_k;
                     stat_k += NCW;
                     return v;
@@ -1059,46 +1092,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);
             if (++st == p.stages) st = 0, phase ^= 1u;
-        }
-        // Rows excluded from the layout (collapsed rank layout: rows with values
-        // closer than eps, or NaN) are evaluated exactly on the fp64 matrix,
-        // one row per CTA in turn: the row is gathered into the (now idle)
-        // first stage buffer with one round of independent loads, then every
-        // thread walks one series from shared memory.
-        // Dirty rows go to the last CTAs first: those carry no tail-split item.
-        const uint32_t rb = G - 1 - blockIdx.x;
-        if (rb < p.n_excl) {
-            const uint32_t nt = NCW * 32;
-            double* rowbuf = reinterpret_cast<double*>(stage_base);
-            const bool fits = size_t(p.n_cols) * sizeof(double) <= size_t(p.stages) * p.stage_bytes;
-            named_bar_sync(1, nt);  // every consumer is done with the stage buffers
-            for (uint32_t i = rb; i < p.n_excl; i += G) {
-                const uint32_t row = __ldg(p.excl_rows + i);
-                const double* col0 = p.matrix + row;
-                if (fits)
-                    for (uint32_t c = threadIdx.x; c < p.n_cols; c += nt)
-                        rowbuf[c] = __ldg(col0 + size_t(c) * p.ld);
-                named_bar_sync(1, nt);
-                for (uint32_t g = threadIdx.x; g < P; g += nt) {
-                    const uint32_t len = wl.slen[g];
-                    const uint32_t* pc = wl.pcols + wl.sstart[g];
-                    auto value = [&](uint32_t k) {
-                        const uint32_t c = pc[k] / Walker::kColBytes;
-                        return fits ? rowbuf[c] : __ldg(col0 + size_t(c) * p.ld);
-                    };
-                    bool ok = true;
-                    if (len > 1) {
-                        double prev = value(0);
-                        for (uint32_t k = 1; k < len; ++k) {
-                            const double cur = value(k);
-                            ok = ok & step_ok<false>(prev, cur, eps);
-                            prev = cur;
-                        }
-                    }
-                    if (ok) atomicAdd(&wl.cnt[g], 1u);
-                }
-                named_bar_sync(1, nt);
-            }
         }
     }
     __syncthreads();
@@ -1266,6 +1259,14 @@ __global__ void __launch_bounds__(256)
         out[at(c, plane)] = v;
     }
     if (COLLAPSED && tid == 0) dirty_out[r] = static_cast<uint8_t>(s_dirty);
+}
+
+// Row-major copy of selected rows of the column-major matrix (one CTA per row).
+__global__ void gather_rows_kernel(const double* __restrict__ mat, size_t ld, uint32_t n_cols,
+                                   const uint32_t* __restrict__ rows, double* __restrict__ out) {
+    const uint32_t r = rows[blockIdx.x];
+    for (uint32_t c = threadIdx.x; c < n_cols; c += blockDim.x)
+        out[size_t(blockIdx.x) * n_cols + c] = mat[size_t(c) * ld + r];
 }
 
 // Sets *flag if any real (non-padding) cell of the column-major matrix is NaN.
