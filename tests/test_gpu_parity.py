@@ -22,7 +22,7 @@ port = oracle.Port()
 # Every count-kernel configuration the library can select: the exact rank
 # tile (default; 1 or 2 planes by eps / NaN presence, 16 or 31 consumer warps),
 # the fp64 tile (rows-per-tile x rows-per-lane), and the unstaged direct kernel.
-KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NCW="32"), dict(EBIC_NO_COLLAPSE="1"), dict(EBIC_SPG="4"),
+KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NCW="24"), dict(EBIC_NCW="32"), dict(EBIC_NO_COLLAPSE="1"), dict(EBIC_SPG="4"),
                    dict(EBIC_SPG="4", EBIC_NO_COLLAPSE="1")] +
                   [dict(EBIC_LAYOUT_F64="1", EBIC_RPG=str(g), EBIC_RPL=str(l))
                    for g in (32, 16, 8, 4) for l in (1, 2)] +
@@ -113,7 +113,7 @@ def test_every_kernel_config_on_traces(cfg, name):
                 assert bits_equal(f, fit)
 
 
-@pytest.mark.parametrize("cfg", KERNEL_CONFIGS[:7] + KERNEL_CONFIGS[9:10] + KERNEL_CONFIGS[-1:], ids=str)
+@pytest.mark.parametrize("cfg", KERNEL_CONFIGS[:8] + KERNEL_CONFIGS[10:11] + KERNEL_CONFIGS[-1:], ids=str)
 def test_edge_cases_vs_oracle(cfg):
     """Ragged row counts, ties, +-0, NaN/inf cells, odd eps values, len-1 series."""
     rng = np.random.default_rng(7)
