@@ -518,7 +518,8 @@ def run_ours(args):
                      "d2h_bytes_per_step": e2e_cpp["d2h_bytes_per_step"],
                      "us_per_step": e2e_cpp["us_per_step"],
                      "caller": "C++ -> ebic_evaluate_population (C ABI), host buffers",
-                     "parity_mismatched_steps": e2e_cpp["mismatched_steps"]} if e2e_cpp else None),
+                     "parity_mismatched_steps": e2e_cpp["mismatched_steps"],
+                     "host_us_breakdown": e2e_cpp.get("host_us")} if e2e_cpp else None),
             "e2e_python_api": ({"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                                 "d2h_bytes_per_step": d2h,
                                 "caller": "Python Evaluator.evaluate_population (ctypes)"}

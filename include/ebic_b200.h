@@ -157,6 +157,12 @@ int ebic_fitness_device(ebic_ctx* ctx, const uint64_t* d_counts, const uint64_t*
  * min(grid, max_ctas) x 8 values; *n_ctas = grid. */
 int ebic_ctx_phase_times(ebic_ctx* ctx, uint64_t* stamps_out, size_t max_ctas, size_t* n_ctas);
 
+/* Diagnostics: mean host-side time (us) per ebic_count_matches /
+ * ebic_evaluate_population call on this context, split into [validate CBF,
+ * stage + H2D submit, kernel launch submit, wait for the completion flag,
+ * copy-out]; *calls_out = number of calls. */
+int ebic_ctx_host_timers(ebic_ctx* ctx, double* mean_us_out, uint64_t* calls_out);
+
 /* ---- row membership (Steps 6-7) ----------------------------------------- */
 
 /* Per-series row bitmasks over the context's rows (words = ceil(n_rows/64),

@@ -55,6 +55,7 @@ SIGNATURES = [
     ("ebic_count_matches_device", C.c_int, [vp, vp, vp, C.c_size_t, C.c_size_t, C.c_double, C.c_uint64, vp, vp, vp]),
     ("ebic_fitness_device", C.c_int, [vp, vp, vp, C.c_size_t, C.c_uint64, vp, vp]),
     ("ebic_ctx_phase_times", C.c_int, [vp, u64p, C.c_size_t, szp]),
+    ("ebic_ctx_host_timers", C.c_int, [vp, f64p, u64p]),
     ("ebic_membership_bits", C.c_int, [vp, szp, u16p, C.c_size_t, C.c_double, C.c_size_t, u64p, u64p, u64p]),
     ("ebic_assign_rows", C.c_int, [vp, u16p, C.c_size_t, C.c_double, u64p, szp]),
     ("ebic_expand_bicluster", C.c_int, [vp, u16p, C.c_size_t, u64p, u8p, C.c_size_t, C.c_int, C.c_size_t, C.c_double, u64p, u8p, szp]),

@@ -111,7 +111,10 @@ int main(int argc, char** argv) {
     double total_s = 0.0;
     uint64_t series = 0, h2d = 0, d2h = 0;
     int bad = 0;
+    double ht0[5] = {0, 0, 0, 0, 0};
+    uint64_t calls0 = 0;
     for (int k = 0; k < warmup + steps; ++k) {
+        if (k == warmup) ebic_ctx_host_timers(ctx, ht0, &calls0);
         const Batch& b = batches[k % batches.size()];
         const size_t P = b.off.size() - 1;
         fit.assign(P, 0.0);
@@ -134,10 +137,17 @@ int main(int argc, char** argv) {
             d2h += P * 16;
         }
     }
+    double ht[5] = {0, 0, 0, 0, 0};
+    uint64_t calls = 0;
+    ebic_ctx_host_timers(ctx, ht, &calls);
+    for (int i = 0; i < 5; ++i)  // means over the timed calls only
+        ht[i] = calls > calls0 ? (ht[i] * calls - ht0[i] * calls0) / double(calls - calls0) : 0.0;
     std::printf("{\"e2e_biclusters_per_s\": %.6e, \"us_per_step\": %.3f, \"steps\": %d, \"series\": %llu, "
-                "\"h2d_bytes_per_step\": %llu, \"d2h_bytes_per_step\": %llu, \"mismatched_steps\": %d}\n",
+                "\"h2d_bytes_per_step\": %llu, \"d2h_bytes_per_step\": %llu, \"mismatched_steps\": %d, "
+                "\"host_us\": {\"validate\": %.2f, \"stage_h2d\": %.2f, \"launch\": %.2f, \"wait\": %.2f, \"copy_out\": %.2f}}\n",
                 series / total_s, total_s / steps * 1e6, steps, (unsigned long long)series,
-                (unsigned long long)(h2d / steps), (unsigned long long)(d2h / steps), bad);
+                (unsigned long long)(h2d / steps), (unsigned long long)(d2h / steps), bad,
+                ht[0], ht[1], ht[2], ht[3], ht[4]);
     ebic_ctx_destroy(ctx);
     return bad ? 3 : 0;
 }

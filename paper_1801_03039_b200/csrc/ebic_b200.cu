@@ -12,6 +12,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -71,7 +72,7 @@ int env_int(const char* name, int dflt) {
 // context is created so the per-generation launch path makes no getenv calls.
 struct Knobs {
     int force_direct, rpg, rpl, stages, ncw, slice, layout_f64, no_collapse, sched_static,
-        max_parts, reduce_tree, grid, phase_timing, spg;
+        max_parts, reduce_tree, grid, phase_timing, spg, host_copy;
     static Knobs from_env() {
         Knobs k;
         k.force_direct = env_int("EBIC_FORCE_DIRECT", 0);
@@ -88,6 +89,7 @@ struct Knobs {
         k.grid = env_int("EBIC_GRID", 0);
         k.phase_timing = env_int("EBIC_PHASE_TIMING", 0);
         k.spg = env_int("EBIC_SPG", 0);
+        k.host_copy = env_int("EBIC_HOST_COPY", 0);
         return k;
     }
 };
@@ -187,13 +189,20 @@ struct Shard {
     // mapped pinned results of host-path launches: [flag (128 B)][counts P][fitness P]
     unsigned char* h_map = nullptr;
     size_t h_map_cap = 0;
+    // mapped pinned staging of the host CBF (read by the device)
+    unsigned char* h_in_map = nullptr;
+    size_t h_in_map_cap = 0;
     unsigned long long seq = 0;
+    uint64_t cbf_seq = 0;
     Tables tables;
     unsigned long long* d_phase = nullptr;  // EBIC_PHASE_TIMING: per-CTA phase stamps
     RankLayout ranks[2];
     uint64_t rank_clock = 0;
     int has_nan = -1;  // -1 unknown
     int last_grid = 0;
+    // host-path phase timers (us, accumulated): validate, stage+H2D, launch, wait, copy-out
+    double host_us[5] = {0, 0, 0, 0, 0};
+    uint64_t host_calls = 0;
     int last_reduce = -1;  // reduction-tail mode of the last launch
     bool last_collapsed = false;
     // choose_config memo (same P / L / layout as the previous launch)
@@ -282,12 +291,12 @@ void upload_shard(Shard& s, const double* src_rows, size_t n_cols, bool src_on_d
     CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     s.ld = std::max<size_t>(64, (s.rows + 63) / 64 * 64);
     CK(cudaMalloc(&s.d_mat, s.ld * n_cols * sizeof(double)));
-    CK(cudaMalloc(&s.d_done, (kMaxGroups + 1) * sizeof(unsigned int)));
+    CK(cudaMalloc(&s.d_done, (kMaxGroups + 2) * sizeof(unsigned int)));
     if (s.knobs.phase_timing) {
         CK(cudaMalloc(&s.d_phase, 4096 * 8 * sizeof(unsigned long long)));
         CK(cudaMemsetAsync(s.d_phase, 0, 4096 * 8 * sizeof(unsigned long long), s.stream));
     }
-    CK(cudaMemsetAsync(s.d_done, 0, (kMaxGroups + 1) * sizeof(unsigned int), s.stream));
+    CK(cudaMemsetAsync(s.d_done, 0, (kMaxGroups + 2) * sizeof(unsigned int), s.stream));
 
     // Stage <= 64 MB of rows at a time (and < 2^21 rows: grid.y limit).
     size_t chunk = std::max<size_t>(32, (64ull << 20) / (n_cols * sizeof(double)));
@@ -661,7 +670,8 @@ const Tables& ensure_tables(Shard& s, uint64_t sigma, size_t total_rows) {
 void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t* d_cols, size_t P,
                   size_t L, double eps, uint64_t* d_counts, double* d_fit, uint64_t sigma,
                   cudaStream_t st, uint64_t cols_base, unsigned long long* done_flag = nullptr,
-                  unsigned long long done_seq = 0) {
+                  unsigned long long done_seq = 0, const void* host_cbf = nullptr,
+                  size_t cbf_bytes = 0) {
     if (P == 0) return;
     if (P > 0xffffffffull || L > 0xffffffffull || s.rows > 0xffffffffull)
         fail(EBIC_ERR_INVALID_ARGUMENT, "population or shard too large for one launch");
@@ -685,6 +695,13 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
     p.reduce_striped = s.knobs.reduce_tree ? 0u : 1u;
     p.done_flag = done_flag;
     p.done_seq = done_seq;
+    if (host_cbf) {
+        p.host_cbf = static_cast<const uint4*>(host_cbf);
+        p.dev_cbf = reinterpret_cast<uint4*>(s.d_in);
+        p.cbf_words = (uint32_t)((cbf_bytes + 15) / 16);
+        p.cbf_ready = s.d_done + kMaxGroups + 1;
+        p.cbf_seq = (unsigned int)++s.cbf_seq;
+    }
     p.phase_ns = s.d_phase;
     if (d_fit) {
         const Tables& t = ensure_tables(s, sigma, ctx.total_rows);
@@ -730,6 +747,10 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
     } else {
         const size_t smem = 8 * P + 16;
         if (smem > (size_t)s.max_smem) fail(EBIC_ERR_INVALID_ARGUMENT, "population too large for one launch");
+        if (p.host_cbf) {  // the direct kernel reads the CBF straight from device memory
+            CK(cudaMemcpyAsync(s.d_in, host_cbf, cbf_bytes, cudaMemcpyHostToDevice, st));
+            p.host_cbf = nullptr;
+        }
         const int grid = (int)((s.rows + 255) / 256);
         s.last_grid = grid;
         s.last_cfg = c;
@@ -784,10 +805,21 @@ void wait_flag(Shard& s, unsigned long long seq) {
     }
 }
 
+using HostClock = std::chrono::steady_clock;
+inline double us_since(HostClock::time_point& t) {
+    const auto n = HostClock::now();
+    const double d = std::chrono::duration<double, std::micro>(n - t).count();
+    t = n;
+    return d;
+}
+
 void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_t P, double eps,
                    bool want_fit, uint64_t sigma, uint64_t* counts_out, double* fit_out) {
     if (P == 0) return;
+    Shard& s0 = ctx.shards[0];
+    auto tp = HostClock::now();
     validate_cbf(off, cols, P, ctx.n_cols);
+    s0.host_us[0] += us_since(tp);
     const size_t L = off[P];
     const size_t off_bytes = (P + 1) * sizeof(uint64_t);
     const size_t cols_at = (off_bytes + 15) & ~size_t(15);
@@ -795,13 +827,20 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
     const bool single = ctx.shards.size() == 1;
     for (Shard& s : ctx.shards) {
         DeviceGuard g(s.device);
-        grow_pinned(&s.h_pin, &s.h_pin_cap, in_bytes + 16);
+        grow_mapped(&s.h_in_map, &s.h_in_map_cap, in_bytes + 64);
         grow_mapped(&s.h_map, &s.h_map_cap, 128 + P * 16);
         grow_device(&s.d_in, &s.d_in_cap, in_bytes + 64);
         static_assert(sizeof(size_t) == sizeof(uint64_t), "size_t must be 64-bit");
-        std::memcpy(s.h_pin, off, off_bytes);
-        if (L) std::memcpy(s.h_pin + cols_at, cols, L * sizeof(uint16_t));
-        CK(cudaMemcpyAsync(s.d_in, s.h_pin, in_bytes, cudaMemcpyHostToDevice, s.stream));
+        // Stage the CBF in mapped pinned memory.  A single TMA launch copies it
+        // to the device itself (CTA 0, stage_host_cbf): no cudaMemcpyAsync on
+        // the per-generation path.  Otherwise one async copy.
+        std::memcpy(s.h_in_map, off, off_bytes);
+        if (L) std::memcpy(s.h_in_map + cols_at, cols, L * sizeof(uint16_t));
+        const bool one_launch = P <= kMaxSeriesPerLaunch && L <= kMaxLenPerLaunch &&
+                                !s.knobs.host_copy;
+        if (!one_launch)
+            CK(cudaMemcpyAsync(s.d_in, s.h_in_map, in_bytes, cudaMemcpyHostToDevice, s.stream));
+        if (&s == &s0) s0.host_us[1] += us_since(tp);
         uint64_t* m_counts = reinterpret_cast<uint64_t*>(s.h_map + 128);
         double* m_fit = (single && want_fit) ? reinterpret_cast<double*>(s.h_map + 128 + P * 8) : nullptr;
         const auto* d_off = reinterpret_cast<const uint64_t*>(s.d_in);
@@ -811,22 +850,25 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
         // kMaxLenPerLaunch columns (the per-CTA work list lives in shared
         // memory); a generation (P ~ 600) is always a single launch.  Only
         // the last launch raises the flag (launches are stream-ordered).
-        for (size_t s0 = 0; s0 < P;) {
-            size_t s1 = s0;
-            while (s1 < P && s1 - s0 < kMaxSeriesPerLaunch && off[s1 + 1] - off[s0] <= kMaxLenPerLaunch) ++s1;
-            if (s1 == s0) s1 = s0 + 1;  // a single over-long series still gets its own launch
-            const bool last = s1 == P;
-            launch_count(ctx, s, d_off + s0, d_cols, s1 - s0, off[s1] - off[s0], eps, m_counts + s0,
-                         m_fit ? m_fit + s0 : nullptr, sigma, s.stream, off[s0],
-                         last ? reinterpret_cast<unsigned long long*>(s.h_map) : nullptr, seq);
-            s0 = s1;
+        for (size_t a = 0; a < P;) {
+            size_t b = a;
+            while (b < P && b - a < kMaxSeriesPerLaunch && off[b + 1] - off[a] <= kMaxLenPerLaunch) ++b;
+            if (b == a) b = a + 1;  // a single over-long series still gets its own launch
+            const bool last = b == P;
+            launch_count(ctx, s, d_off + a, d_cols, b - a, off[b] - off[a], eps, m_counts + a,
+                         m_fit ? m_fit + a : nullptr, sigma, s.stream, off[a],
+                         last ? reinterpret_cast<unsigned long long*>(s.h_map) : nullptr, seq,
+                         one_launch ? s.h_in_map : nullptr, in_bytes);
+            a = b;
         }
+        if (&s == &s0) s0.host_us[2] += us_since(tp);
     }
     std::vector<uint64_t> total;
     if (!single) total.assign(P, 0);
     for (Shard& s : ctx.shards) {
         DeviceGuard g(s.device);
         wait_flag(s, s.seq);
+        if (&s == &s0) s0.host_us[3] += us_since(tp);
         const uint64_t* c = reinterpret_cast<const uint64_t*>(s.h_map + 128);
         if (single) {
             if (counts_out) std::memcpy(counts_out, c, P * 8);
@@ -841,6 +883,8 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
             for (size_t p = 0; p < P; ++p)
                 fit_out[p] = ebic_fitness_score(total[p], off[p + 1] - off[p], sigma);
     }
+    s0.host_us[4] += us_since(tp);
+    ++s0.host_calls;
 }
 
 // Membership bitmasks of every shard gathered into global word order.
@@ -904,6 +948,7 @@ void free_shard(Shard& s) {
     cudaFree(s.d_out);
     if (s.h_pin) cudaFreeHost(s.h_pin);
     if (s.h_map) cudaFreeHost(s.h_map);
+    if (s.h_in_map) cudaFreeHost(s.h_in_map);
     cudaFree(s.tables.d_log);
     cudaFree(s.tables.d_exp);
     for (RankLayout& rl : s.ranks) {
@@ -1135,6 +1180,15 @@ int ebic_ctx_phase_times(ebic_ctx* ctx, uint64_t* stamps_out, size_t max_ctas, s
         const size_t n = std::min<size_t>(max_ctas, (size_t)s.last_grid);
         CK(cudaDeviceSynchronize());
         CK(cudaMemcpy(stamps_out, s.d_phase, n * 8 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    });
+}
+
+int ebic_ctx_host_timers(ebic_ctx* ctx, double* mean_us_out, uint64_t* calls_out) {
+    return guarded([&] {
+        if (!ctx || !mean_us_out) fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+        const Shard& s = ctx->shards[0];
+        for (int i = 0; i < 5; ++i) mean_us_out[i] = s.host_calls ? s.host_us[i] / s.host_calls : 0.0;
+        if (calls_out) *calls_out = s.host_calls;
     });
 }
 

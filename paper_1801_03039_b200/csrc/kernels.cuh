@@ -171,6 +171,15 @@ struct CountParams {
     // them system-visible and stores done_seq to *done_flag.
     unsigned long long* done_flag;
     unsigned long long done_seq;
+    // Optional host-resident CBF (mapped pinned memory, device-visible): CTA 0
+    // copies cbf_bytes from host_cbf to dev_cbf (where offsets / cols point)
+    // and publishes cbf_seq in *cbf_ready; the other CTAs wait for it.  This
+    // replaces a host cudaMemcpyAsync (several us of API time per call).
+    const uint4* __restrict__ host_cbf;
+    uint4* __restrict__ dev_cbf;
+    uint32_t cbf_words;                    // 16-byte words to copy
+    unsigned int* __restrict__ cbf_ready;
+    unsigned int cbf_seq;
     uint64_t table_n;                      // entries of logt/expt (prefetched into L2)
     unsigned long long* __restrict__ phase_ns;  // optional [grid][8] %globaltimer stamps
 };
@@ -336,8 +345,10 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
             const uint32_t i = s0 + k * nthreads;
-            if (i <= P) o[k] = __ldg(p.offsets + i);
-            if (i < n_vec) v[k] = __ldg(vsrc + i);
+            // L2-coherent loads: the CBF may have been staged by CTA 0 during
+            // this launch (stage_host_cbf), which the read-only path may miss.
+            if (i <= P) o[k] = __ldcg(p.offsets + i);
+            if (i < n_vec) v[k] = __ldcg(vsrc + i);
         }
 #pragma unroll
         for (int k = 0; k < kPer; ++k) {
@@ -885,6 +896,30 @@ struct RankWalker {
     }
 };
 
+// Host-resident CBF (see CountParams::host_cbf): CTA 0's consumers copy it
+// into device memory with one round of 16-byte PCIe reads and publish a
+// release flag; every other CTA acquires it.  CTAs are launched in index
+// order, so CTA 0 is resident whenever another CTA waits here.
+__device__ __forceinline__ void stage_host_cbf(const CountParams& p, int tid, int nthreads,
+                                               int bar_id) {
+    if (blockIdx.x == 0) {
+        for (uint32_t i = tid; i < p.cbf_words; i += nthreads) p.dev_cbf[i] = p.host_cbf[i];
+        __threadfence();
+        named_bar_sync(bar_id, nthreads);
+        if (tid == 0)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.cbf_ready), "r"(p.cbf_seq)
+                         : "memory");
+    } else {
+        if (tid == 0) {
+            uint32_t v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.cbf_ready) : "memory");
+            } while (v != p.cbf_seq);
+        }
+        named_bar_sync(bar_id, nthreads);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K1: TMA-staged count kernel.
 //
@@ -994,6 +1029,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         }
     } else {
         // ---------------- consumer warps ----------------
+        if (p.host_cbf) stage_host_cbf(p, threadIdx.x, NCW * 32, 1);
         build_work_list(p, wl, threadIdx.x, NCW * 32, 1, Walker::kColBytes);
         if (threadIdx.x == 0) mbar_arrive(prol_bar);
         if (stamp && threadIdx.x == 0) stamp[1] = global_ns();
