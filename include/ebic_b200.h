@@ -206,6 +206,28 @@ int ebic_synth_generate(size_t n_rows, size_t n_cols, size_t n_blocks, const siz
                         const size_t* block_cols, int pattern, size_t overlap_rows,
                         size_t overlap_cols, double noise_sd, uint64_t seed, double* values_out);
 
+/* ---- top-rank admission (evolution.hpp:168-206) ------------------------- */
+
+/* Replaces TopRankList::update (evolution.hpp:168-206), host only, stateless.
+ * Current entries (n_entries series in CBF form with their fitness and seq)
+ * are offered the n_cand candidates exactly as the reference does: positive
+ * fitness only, visited by fitness desc / index asc; a candidate is blocked by
+ * any entry of >= fitness overlapping it above overlap_threshold
+ * (|a & b| / min(|a|, |b|), evolution.hpp:154-160), otherwise it evicts the
+ * overlapping lower-fitness entries and is appended with seq = (*next_seq)++.
+ * The survivors sorted by (fitness desc, seq asc) and truncated to capacity
+ * are written as out_ref[i] (>= 0: entry index, < 0: candidate -(ref + 1))
+ * and out_seq[i]; *out_count <= min(capacity, n_entries + n_cand) (size the
+ * outputs for that).  Like the reference's update, threshold and capacity
+ * are not validated (run() does that, evolution.hpp:45-49); columns must be
+ * < n_cols. */
+int ebic_top_rank_update(size_t n_cols, size_t n_entries, const size_t* entry_offsets,
+                         const uint16_t* entry_cols, const double* entry_fitness,
+                         const uint64_t* entry_seq, size_t n_cand, const size_t* cand_offsets,
+                         const uint16_t* cand_cols, const double* cand_fitness,
+                         double overlap_threshold, size_t capacity, uint64_t* next_seq,
+                         int64_t* out_ref, uint64_t* out_seq, size_t* out_count);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

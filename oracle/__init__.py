@@ -32,6 +32,7 @@ u16p = C.POINTER(C.c_uint16)
 u64p = C.POINTER(C.c_uint64)
 f64p = C.POINTER(C.c_double)
 szp = C.POINTER(C.c_size_t)
+i64p = C.POINTER(C.c_int64)
 
 
 def build(ref: bool = True) -> None:
@@ -71,6 +72,10 @@ class Port:
         L.orc_membership_bits.argtypes = [f64p, C.c_size_t, C.c_size_t, u16p, C.c_size_t, C.c_double,
                                           C.c_size_t, u64p, u64p, u64p]
         L.orc_expand_bicluster.restype = C.c_size_t
+        L.orc_top_rank_update.restype = C.c_int
+        L.orc_top_rank_update.argtypes = [C.c_size_t, C.c_size_t, szp, u16p, f64p, u64p, C.c_size_t,
+                                          szp, u16p, f64p, C.c_double, C.c_size_t, u64p, i64p,
+                                          u64p, szp]
         L.orc_expand_bicluster.argtypes = [f64p, C.c_size_t, C.c_size_t, u16p, C.c_size_t, u64p, u8p,
                                            C.c_size_t, C.c_int, C.c_size_t, C.c_double, u64p, u8p]
         self.lib = L
@@ -156,6 +161,31 @@ class Port:
         return [int(r) for r in ro[:n]], [int(f) for f in fo[:n]]
 
 
+    def top_rank_update(self, n_cols, entries, cand_off, cand_cols, cand_fit, threshold, capacity,
+                        next_seq):
+        """evolution.hpp:168-206 in the stateless ebic_top_rank_update form.
+        entries = (offsets, cols, fitness, seq) arrays.  Returns (ref, seq, next_seq)."""
+        e_off, e_cols, e_fit, e_seq = (np.ascontiguousarray(entries[0], dtype=np.uint64),
+                                       np.ascontiguousarray(entries[1], dtype=np.uint16),
+                                       np.ascontiguousarray(entries[2], dtype=np.float64),
+                                       np.ascontiguousarray(entries[3], dtype=np.uint64))
+        k_off = np.ascontiguousarray(cand_off, dtype=np.uint64)
+        k_cols = np.ascontiguousarray(cand_cols, dtype=np.uint16)
+        k_fit = np.ascontiguousarray(cand_fit, dtype=np.float64)
+        pad = lambda a: a if a.size else np.zeros(1, dtype=a.dtype)  # noqa: E731
+        n_e, n_c = len(e_fit), len(k_fit)
+        cap = max(1, min(capacity, n_e + n_c))
+        ref = np.zeros(cap, dtype=np.int64)
+        seq = np.zeros(cap, dtype=np.uint64)
+        nxt = C.c_uint64(next_seq)
+        n = C.c_size_t(0)
+        self.lib.orc_top_rank_update(n_cols, n_e, _p(e_off, szp), _p(pad(e_cols), u16p),
+                                     _p(pad(e_fit), f64p), _p(pad(e_seq), u64p), n_c, _p(k_off, szp),
+                                     _p(pad(k_cols), u16p), _p(pad(k_fit), f64p), float(threshold),
+                                     capacity, C.byref(nxt), _p(ref, i64p), _p(seq, u64p), C.byref(n))
+        return ref[:n.value], seq[:n.value], nxt.value
+
+
 class Ref:
     """ctypes view of oracle/_ref/libebic_ref.so (reference headers, compiled here)."""
 
@@ -186,6 +216,21 @@ class Ref:
                                    C.c_size_t, C.c_size_t, C.c_double, C.c_uint64, f64p]
         L.ref_derive_seed.restype = C.c_uint64
         L.ref_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.ref_toprank_create.restype = C.c_void_p
+        L.ref_toprank_create.argtypes = [C.c_size_t]
+        L.ref_toprank_destroy.argtypes = [C.c_void_p]
+        L.ref_toprank_update.argtypes = [C.c_void_p, szp, u16p, C.c_size_t, f64p, C.c_double,
+                                         C.c_size_t]
+        L.ref_toprank_size.restype = C.c_size_t
+        L.ref_toprank_size.argtypes = [C.c_void_p]
+        L.ref_toprank_entries.restype = C.c_size_t
+        L.ref_toprank_entries.argtypes = [C.c_void_p, szp, u16p, f64p, u64p]
+        L.ref_toprank_time.restype = C.c_double
+        L.ref_toprank_time.argtypes = [C.c_size_t, C.c_size_t, szp, szp, u16p, f64p, C.c_double,
+                                       C.c_size_t, C.c_int]
+        L.ref_run_population_trace.restype = C.c_long
+        L.ref_run_population_trace.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, C.c_uint64,
+                                               C.c_double, C.c_uint64, C.c_uint, C.c_char_p]
         L.ref_run_trace.restype = C.c_long
         L.ref_run_trace.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, C.c_uint64, C.c_double,
                                     C.c_uint64, C.c_uint, C.c_size_t, C.c_char_p]
@@ -267,6 +312,81 @@ class Ref:
         if n < 0:
             raise RuntimeError("reference run failed")
         return n
+
+
+    class TopRank:
+        """The reference's own TopRankList (evolution.hpp:142-218)."""
+
+        def __init__(self, ref, n_cols):
+            self.ref = ref
+            self.h = ref.lib.ref_toprank_create(n_cols)
+
+        def __del__(self):
+            try:
+                self.ref.lib.ref_toprank_destroy(self.h)
+            except Exception:
+                pass
+
+        def update(self, off, cols, fit, threshold=0.75, capacity=100):
+            off = np.ascontiguousarray(off, dtype=np.uint64)
+            cols = np.ascontiguousarray(cols, dtype=np.uint16)
+            fit = np.ascontiguousarray(fit, dtype=np.float64)
+            pad = lambda a: a if a.size else np.zeros(1, dtype=a.dtype)  # noqa: E731
+            self.ref.lib.ref_toprank_update(self.h, _p(off, szp), _p(pad(cols), u16p), len(fit),
+                                            _p(pad(fit), f64p), float(threshold), capacity)
+
+        def entries(self):
+            """-> (offsets u64, cols u16, fitness f64, seq u64)."""
+            L = self.ref.lib
+            n = L.ref_toprank_size(self.h)
+            total = L.ref_toprank_entries(self.h, None, None, None, None)
+            off = np.zeros(n + 1, dtype=np.uint64)
+            cols = np.zeros(max(total, 1), dtype=np.uint16)
+            fit = np.zeros(max(n, 1), dtype=np.float64)
+            seq = np.zeros(max(n, 1), dtype=np.uint64)
+            L.ref_toprank_entries(self.h, _p(off, szp), _p(cols, u16p), _p(fit, f64p), _p(seq, u64p))
+            return off, cols[:total], fit[:n], seq[:n]
+
+    def run_population_trace(self, m, path, population=600, iterations=10, rng_seed=1, eps=0.0,
+                             sigma=0, threads=1):
+        n = self.lib.ref_run_population_trace(m.h, population, iterations, rng_seed, float(eps),
+                                              sigma, threads, str(path).encode())
+        if n < 0:
+            raise RuntimeError("reference run failed")
+        return n
+
+    def top_rank(self, n_cols):
+        return Ref.TopRank(self, n_cols)
+
+    def top_rank_time(self, n_cols, updates, threshold=0.75, capacity=100, reps=3):
+        """Mean us per TopRankList::update replaying [(off, cols, fit), ...]."""
+        sizes = np.array([len(f) for _, _, f in updates], dtype=np.uint64)
+        offs, colss, fits, base = [np.zeros(1, dtype=np.uint64)], [], [], 0
+        for off, cols, fit in updates:
+            offs.append(np.asarray(off[1:], dtype=np.uint64) + base)
+            base += int(off[-1])
+            colss.append(np.asarray(cols, dtype=np.uint16))
+            fits.append(np.asarray(fit, dtype=np.float64))
+        off = np.concatenate(offs)
+        cols = np.concatenate(colss)
+        fit = np.concatenate(fits)
+        return self.lib.ref_toprank_time(n_cols, len(updates), _p(sizes, szp), _p(off, szp),
+                                         _p(cols, u16p), _p(fit, f64p), float(threshold), capacity,
+                                         reps)
+
+
+def read_population_trace(path):
+    """Parse a ref_run_population_trace file -> list of (offsets u64, cols u16, fitness f64)."""
+    data = Path(path).read_bytes()
+    at, out = 0, []
+    while at < len(data):
+        P = int(np.frombuffer(data, np.uint64, 1, at)[0]); at += 8
+        off = np.frombuffer(data, np.uint64, P + 1, at).copy(); at += 8 * (P + 1)
+        L = int(off[-1])
+        cols = np.frombuffer(data, np.uint16, L, at).copy(); at += 2 * L
+        fit = np.frombuffer(data, np.float64, P, at).copy(); at += 8 * P
+        out.append((off, cols, fit))
+    return out
 
 
 def read_trace(path):

@@ -213,3 +213,109 @@ ORC_EXPORT size_t orc_expand_bicluster(const double* values, size_t n_rows, size
     free(rev);
     return n;
 }
+
+/* ---- top-rank admission (evolution.hpp:132-218, TopRankList) ----------- */
+
+typedef struct {
+    int64_t ref;     /* >= 0 entry index, < 0 -(candidate + 1) */
+    double fitness;
+    uint64_t seq;
+    size_t len;      /* series.size() */
+    uint64_t* mask;  /* column mask, (n_cols + 63) / 64 words (:208-213) */
+} orc_tr_entry;
+
+static const double* g_tr_fit; /* qsort context (single-threaded oracle) */
+
+/* :176-179 -- fitness desc, then population index asc. */
+static int orc_tr_order_cmp(const void* a, const void* b) {
+    size_t x = *(const size_t*)a, y = *(const size_t*)b;
+    if (g_tr_fit[x] != g_tr_fit[y]) return g_tr_fit[x] > g_tr_fit[y] ? -1 : 1;
+    return x < y ? -1 : (x > y);
+}
+
+/* :201-204 -- fitness desc, then seq asc. */
+static int orc_tr_entry_cmp(const void* a, const void* b) {
+    const orc_tr_entry* x = (const orc_tr_entry*)a;
+    const orc_tr_entry* y = (const orc_tr_entry*)b;
+    if (x->fitness != y->fitness) return x->fitness > y->fitness ? -1 : 1;
+    return x->seq < y->seq ? -1 : (x->seq > y->seq);
+}
+
+/* :154-160 -- shared columns as a fraction of the smaller series. */
+static double orc_tr_overlap(const orc_tr_entry* a, const orc_tr_entry* b, size_t words) {
+    uint64_t inter = 0;
+    for (size_t w = 0; w < words; ++w) inter += (uint64_t)__builtin_popcountll(a->mask[w] & b->mask[w]);
+    size_t m = a->len < b->len ? a->len : b->len;
+    return (double)inter / (double)m;
+}
+
+static void orc_tr_fill(orc_tr_entry* e, const uint16_t* cols, size_t len, size_t words) {
+    e->len = len;
+    e->mask = (uint64_t*)calloc(words ? words : 1, sizeof(uint64_t));
+    for (size_t i = 0; i < len; ++i) e->mask[cols[i] / 64] |= (uint64_t)1 << (cols[i] % 64);
+}
+
+/* evolution.hpp:168-206 (TopRankList::update) in the stateless form of
+ * ebic_top_rank_update (include/ebic_b200.h): the list starts as the given
+ * entries in the given order; output out_ref/out_seq in final order. */
+ORC_EXPORT int orc_top_rank_update(size_t n_cols, size_t n_entries, const size_t* eoff,
+                                   const uint16_t* ecols, const double* efit, const uint64_t* eseq,
+                                   size_t n_cand, const size_t* coff, const uint16_t* ccols,
+                                   const double* cfit, double thr, size_t capacity,
+                                   uint64_t* next_seq, int64_t* out_ref, uint64_t* out_seq,
+                                   size_t* out_count) {
+    size_t words = (n_cols + 63) / 64;
+    orc_tr_entry* list = (orc_tr_entry*)malloc((n_entries + n_cand + 1) * sizeof(orc_tr_entry));
+    size_t n = 0;
+    for (size_t e = 0; e < n_entries; ++e, ++n) {
+        list[n].ref = (int64_t)e;
+        list[n].fitness = efit[e];
+        list[n].seq = eseq[e];
+        orc_tr_fill(&list[n], ecols + eoff[e], eoff[e + 1] - eoff[e], words);
+    }
+    size_t* order = (size_t*)malloc((n_cand + 1) * sizeof(size_t));
+    size_t n_order = 0;
+    for (size_t i = 0; i < n_cand; ++i)
+        if (cfit[i] > 0.0) order[n_order++] = i; /* :172-175 */
+    g_tr_fit = cfit;
+    qsort(order, n_order, sizeof(size_t), orc_tr_order_cmp);
+
+    for (size_t k = 0; k < n_order; ++k) {
+        size_t i = order[k];
+        orc_tr_entry cand;
+        cand.ref = -(int64_t)i - 1;
+        cand.fitness = cfit[i];
+        orc_tr_fill(&cand, ccols + coff[i], coff[i + 1] - coff[i], words);
+        int blocked = 0; /* :185-192 */
+        for (size_t e = 0; e < n && !blocked; ++e)
+            if (list[e].fitness >= cand.fitness && orc_tr_overlap(&list[e], &cand, words) > thr)
+                blocked = 1;
+        if (blocked) {
+            free(cand.mask);
+            continue;
+        }
+        size_t kept = 0; /* std::erase_if, order preserving (:194-196) */
+        for (size_t e = 0; e < n; ++e) {
+            if (list[e].fitness < cand.fitness && orc_tr_overlap(&list[e], &cand, words) > thr)
+                free(list[e].mask);
+            else
+                list[kept++] = list[e];
+        }
+        n = kept;
+        cand.seq = (*next_seq)++; /* :197-198 */
+        list[n++] = cand;
+    }
+    qsort(list, n, sizeof(orc_tr_entry), orc_tr_entry_cmp); /* :201-204 */
+    size_t keep = n < capacity ? n : capacity;              /* :205 */
+    for (size_t e = 0; e < n; ++e) {
+        if (e < keep) {
+            out_ref[e] = list[e].ref;
+            out_seq[e] = list[e].seq;
+        }
+        free(list[e].mask);
+    }
+    *out_count = keep;
+    free(order);
+    free(list);
+    return 0;
+}

@@ -8,6 +8,8 @@
 // the reference CPU arm (`--impl reference`, cpu_baseline kind "reference").
 // Built by oracle/Makefile only when /root/reference is present.
 #include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
@@ -244,6 +246,137 @@ void ref_fixture_random_matrix(std::size_t rows, std::size_t cols, std::uint64_t
                                double* values_out) {
     Rng rng(seed);
     for (std::size_t i = 0; i < rows * cols; ++i) values_out[i] = rng.normal(0.0, 1.0);
+}
+
+// Runs the reference GA and records, per generation, the whole population and
+// fitness vector that TopRankList::update receives (evolution.hpp:487, :513):
+// gen 0 = the initial population; gen g = the elite clones of the previous
+// top-rank list (build_generation, :394-402) followed by the novel series
+// (on_evaluate, :503) with their evaluated fitness.  File layout: repeated
+// { u64 P; u64 offsets[P+1]; u16 cols[offsets[P]]; f64 fitness[P] }.
+long ref_run_population_trace(void* h, std::size_t population, std::size_t iterations,
+                              std::uint64_t rng_seed, double eps, std::uint64_t sigma,
+                              unsigned threads, const char* path) {
+    const auto& m = *static_cast<ExpressionMatrix*>(h);
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) return -1;
+    RunConfig cfg;
+    cfg.evo.population_size = population;
+    cfg.evo.max_iterations = iterations;
+    cfg.evo.rng_seed = rng_seed;
+    cfg.epsilon = eps;
+    cfg.sigma = sigma;
+    cfg.threads = threads;
+    const ChunkPlan plan = make_chunk_plan(m.n_rows, threads);
+    FitnessParams params;
+    params.sigma = sigma != 0 ? sigma : default_sigma(m.n_rows);
+    std::vector<TopRankEntry> prev_top;
+    std::vector<ColumnSeries> novel;
+    long recorded = 0;
+    RunHooks hooks;
+    hooks.on_evaluate = [&](std::span<const ColumnSeries> s) { novel.assign(s.begin(), s.end()); };
+    hooks.on_generation = [&](std::size_t gen, const TopRankList& top) {
+        std::vector<ColumnSeries> pop;
+        std::vector<double> fit;
+        if (gen > 0) {
+            const std::size_t elites = std::min<std::size_t>(
+                static_cast<std::size_t>(std::ceil(cfg.evo.elite_fraction * double(prev_top.size()))),
+                population);
+            for (std::size_t e = 0; e < elites; ++e) {
+                pop.push_back(prev_top[e].series);
+                fit.push_back(prev_top[e].fitness);
+            }
+        }
+        if (!novel.empty()) {
+            const auto nf = evaluate_population(m, encode_population(novel), plan, params, eps);
+            pop.insert(pop.end(), novel.begin(), novel.end());
+            fit.insert(fit.end(), nf.begin(), nf.end());
+        }
+        novel.clear();
+        const CbfPopulation cbf = encode_population(pop);
+        const std::uint64_t p = cbf.size();
+        std::fwrite(&p, sizeof p, 1, f);
+        std::vector<std::uint64_t> off(cbf.offsets.begin(), cbf.offsets.end());
+        std::fwrite(off.data(), sizeof(std::uint64_t), off.size(), f);
+        std::fwrite(cbf.col_indices.data(), sizeof(std::uint16_t), cbf.col_indices.size(), f);
+        std::fwrite(fit.data(), sizeof(double), fit.size(), f);
+        prev_top = top.entries();
+        ++recorded;
+    };
+    try {
+        (void)run(m, cfg, hooks);
+    } catch (...) {
+        std::fclose(f);
+        return -1;
+    }
+    std::fclose(f);
+    return recorded;
+}
+
+// ---- TopRankList (inc/evolution.hpp:142-218), driven through its public API ----
+
+void* ref_toprank_create(std::size_t n_cols) { return new TopRankList(n_cols); }
+void ref_toprank_destroy(void* h) { delete static_cast<TopRankList*>(h); }
+
+// One TopRankList::update (:168-206) over a CBF population.
+int ref_toprank_update(void* h, const std::size_t* offsets, const std::uint16_t* cols, std::size_t n,
+                       const double* fitness, double overlap_threshold, std::size_t capacity) {
+    auto& t = *static_cast<TopRankList*>(h);
+    std::vector<ColumnSeries> pop;
+    pop.reserve(n);
+    for (std::size_t i = 0; i < n; ++i) pop.emplace_back(cols + offsets[i], cols + offsets[i + 1]);
+    EvolutionConfig cfg;
+    cfg.overlap_threshold = overlap_threshold;
+    cfg.top_rank_capacity = capacity;
+    t.update(pop, std::span<const double>(fitness, n), cfg);
+    return 0;
+}
+
+std::size_t ref_toprank_size(void* h) { return static_cast<TopRankList*>(h)->size(); }
+
+// entries() (:148) as CBF + fitness + seq; offsets_out has size()+1 slots,
+// cols_out capacity = total columns (query with cols_out == nullptr).
+std::size_t ref_toprank_entries(void* h, std::size_t* offsets_out, std::uint16_t* cols_out,
+                                double* fitness_out, std::uint64_t* seq_out) {
+    const auto& es = static_cast<TopRankList*>(h)->entries();
+    std::size_t total = 0;
+    for (std::size_t i = 0; i < es.size(); ++i) {
+        if (offsets_out) offsets_out[i] = total;
+        if (cols_out) std::copy(es[i].series.begin(), es[i].series.end(), cols_out + total);
+        if (fitness_out) fitness_out[i] = es[i].fitness;
+        if (seq_out) seq_out[i] = es[i].seq;
+        total += es[i].series.size();
+    }
+    if (offsets_out) offsets_out[es.size()] = total;
+    return total;
+}
+
+// Times n_updates TopRankList::update calls replaying a recorded sequence
+// (the reference arm of the top-rank microbenchmark).  Populations are CBF
+// slices pop_offsets[u]..; returns mean microseconds per update.
+double ref_toprank_time(std::size_t n_cols, std::size_t n_updates, const std::size_t* pop_sizes,
+                        const std::size_t* offsets, const std::uint16_t* cols, const double* fitness,
+                        double overlap_threshold, std::size_t capacity, int reps) {
+    std::vector<std::vector<ColumnSeries>> pops(n_updates);
+    std::size_t s = 0;
+    for (std::size_t u = 0; u < n_updates; ++u)
+        for (std::size_t i = 0; i < pop_sizes[u]; ++i, ++s)
+            pops[u].emplace_back(cols + offsets[s], cols + offsets[s + 1]);
+    EvolutionConfig cfg;
+    cfg.overlap_threshold = overlap_threshold;
+    cfg.top_rank_capacity = capacity;
+    double total = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        TopRankList t(n_cols);
+        std::size_t f0 = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (std::size_t u = 0; u < n_updates; ++u) {
+            t.update(pops[u], std::span<const double>(fitness + f0, pop_sizes[u]), cfg);
+            f0 += pop_sizes[u];
+        }
+        total += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    }
+    return total / (double(reps) * double(n_updates));
 }
 
 }  // extern "C"

@@ -9,15 +9,17 @@
 //   oracle/_ref/ebic_ref_run     -I /root/reference/proj/include only
 //                                (pure reference CPU path)
 //   oracle/_ref/ebic_dropin_run  -I include  -I /root/reference/proj/include
-//                                i.e. the repo's include/ebic/fitness.hpp and
-//                                include/ebic/expansion.hpp shadow the
-//                                reference's, so the reference's own run() and
-//                                finalize_biclusters() call the B200 library.
+//                                i.e. the repo's include/ebic/{fitness,expansion,
+//                                evolution}.hpp shadow the reference's, so the
+//                                GA loop, top-rank list and the reference's own
+//                                finalize_biclusters() run on the B200 library.
 // tests/test_gpu_dropin.py requires the two JSON files to be byte-identical.
 //
+// Prints the phase wall times (generate / run / finalize / write, ms) on stderr.
 // Usage: run_driver key=value ... out=<path>
 //   rows cols blocks=RxC[,RxC...] pattern overlap seed population iterations
 //   rng_seed epsilon overlap_threshold threads sigma
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -64,7 +66,13 @@ int main(int argc, char** argv) {
         spec.overlap_rows = spec.overlap_cols = std::stoull(kv["overlap"]);
         spec.noise_sd = std::stod(kv["noise"]);
         spec.seed = std::stoull(kv["seed"]);
+        using clk = std::chrono::steady_clock;
+        auto ms = [](clk::time_point a, clk::time_point b) {
+            return std::chrono::duration<double, std::milli>(b - a).count();
+        };
+        const auto t0 = clk::now();
         const GeneratedScenario data = generate(spec);
+        const auto t1 = clk::now();
 
         RunConfig cfg;
         cfg.evo.population_size = std::stoull(kv["population"]);
@@ -75,6 +83,7 @@ int main(int argc, char** argv) {
         cfg.threads = static_cast<unsigned>(std::stoul(kv["threads"]));
         cfg.sigma = std::stoull(kv["sigma"]);
         const RunResult result = run(data.matrix, cfg);
+        const auto t2 = clk::now();
 
         ExpansionOptions exp;
         exp.allow_negative = kv["allow_negative"] != "0";
@@ -83,6 +92,7 @@ int main(int argc, char** argv) {
         if (kv["threshold"] == "none") out_opts.threshold = OutputOptions::Threshold::kNone;
         const std::vector<Bicluster> biclusters = finalize_biclusters(
             result.top_rank, data.matrix, exp, cfg.epsilon, out_opts, result.sigma_used);
+        const auto t3 = clk::now();
 
         RunSummary summary;
         summary.generations = result.generations;
@@ -90,6 +100,9 @@ int main(int argc, char** argv) {
         summary.sigma = result.sigma_used;
         summary.tabu_terminated = result.tabu_terminated;
         write_biclusters_file(kv["out"], biclusters, &summary);
+        const auto t4 = clk::now();
+        std::fprintf(stderr, "[%s] timing_ms generate=%.3f run=%.3f finalize=%.3f write=%.3f\n",
+                     EBIC_DRIVER_NAME, ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
         std::fprintf(stderr, "[%s] generations=%zu series_evaluated=%llu biclusters=%zu\n",
                      EBIC_DRIVER_NAME, result.generations,
                      static_cast<unsigned long long>(result.series_evaluated), biclusters.size());

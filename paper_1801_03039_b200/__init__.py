@@ -21,8 +21,8 @@ from typing import Iterable, List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (CtxInfo, EbicError, check, f64p, fast_count, fast_evaluate, lib, ptr, szp,
-                   u8p, u16p, u64p)
+from ._lib import (CtxInfo, EbicError, check, f64p, fast_count, fast_evaluate, i64p, lib, ptr,
+                   szp, u8p, u16p, u64p)
 
 __all__ = [
     "ExpressionMatrix", "CbfPopulation", "ColumnSeries", "RowRange", "ChunkPlan", "FitnessParams",
@@ -31,7 +31,7 @@ __all__ = [
     "decode_population", "make_chunk_plan", "default_sigma", "fitness_score", "row_matches",
     "count_matches", "evaluate_population", "assign_rows", "trend_violations",
     "resolve_bicluster", "expand_bicluster", "finalize_biclusters", "Evaluator", "synth_generate",
-    "device_count", "shard_range",
+    "device_count", "shard_range", "TopRankEntry", "TopRankList",
 ]
 
 ColumnSeries = List[int]
@@ -499,6 +499,103 @@ def finalize_biclusters(entries: Sequence[tuple], m: ExpressionMatrix, expansion
     res = _evaluator_for(m).resolve_expand_batch([s for s, _ in kept], expansion, epsilon)
     return [Bicluster([int(r) for r in rows], s, f, [RowFlag(int(x)) for x in flags])
             for (s, f), (rows, flags) in zip(kept, res)]
+
+
+# ---------------------------------------------------------------------------
+# Top-rank list (evolution.hpp:132-218) -- host, exact, via ebic_top_rank_update
+# ---------------------------------------------------------------------------
+@dataclass
+class TopRankEntry:  # evolution.hpp:132-137
+    series: List[int]
+    fitness: float
+    seq: int
+
+
+class TopRankList:
+    """Best biclusters found so far (evolution.hpp:142-218).
+
+    Same admission / eviction / tie semantics as the reference's
+    ``TopRankList::update`` (:168-206), computed by ``ebic_top_rank_update``
+    (posting-list overlap counting in libebic_b200.so).  The list is held as
+    CBF arrays so an update passes it to the library without re-encoding.
+    """
+
+    def __init__(self, n_cols: int):
+        self.n_cols = int(n_cols)
+        self._off = np.zeros(1, dtype=np.uint64)
+        self._cols = np.zeros(0, dtype=np.uint16)
+        self._fit = np.zeros(0, dtype=np.float64)
+        self._seq = np.zeros(0, dtype=np.uint64)
+        self._next_seq = C.c_uint64(0)
+
+    def size(self) -> int:
+        return len(self._fit)
+
+    __len__ = size
+
+    def empty(self) -> bool:
+        return len(self._fit) == 0
+
+    def best_fitness(self) -> float:  # :151
+        return float(self._fit[0]) if len(self._fit) else 0.0
+
+    @property
+    def entries(self) -> List[TopRankEntry]:
+        return [TopRankEntry([int(c) for c in self._cols[int(self._off[i]):int(self._off[i + 1])]],
+                             float(self._fit[i]), int(self._seq[i])) for i in range(len(self._fit))]
+
+    @staticmethod
+    def overlap(a: Sequence[int], b: Sequence[int]) -> float:  # :154-160
+        return len(set(int(x) for x in a) & set(int(x) for x in b)) / min(len(a), len(b))
+
+    def update(self, population, fitness, overlap_threshold: float = 0.75,
+               top_rank_capacity: int = 100) -> None:
+        """:168-206.  ``population`` is a CbfPopulation or a sequence of series;
+        ``overlap_threshold`` may also be an EvolutionConfig-like object."""
+        if hasattr(overlap_threshold, "overlap_threshold"):
+            cfg = overlap_threshold
+            overlap_threshold, top_rank_capacity = cfg.overlap_threshold, cfg.top_rank_capacity
+        if not isinstance(population, CbfPopulation):
+            lens = np.fromiter((len(s) for s in population), dtype=np.uint64, count=len(population))
+            off = np.zeros(len(population) + 1, dtype=np.uint64)
+            np.cumsum(lens, out=off[1:])
+            cols = np.fromiter((int(c) for s in population for c in s), dtype=np.uint16,
+                               count=int(off[-1]))
+            population = CbfPopulation(off, cols)
+        c_off = np.ascontiguousarray(population.offsets, dtype=np.uint64)
+        c_cols = np.ascontiguousarray(population.col_indices, dtype=np.uint16)
+        fit = np.ascontiguousarray(fitness, dtype=np.float64)
+        n_cand = len(c_off) - 1
+        if len(fit) != n_cand:
+            raise ValueError("fitness and population sizes differ")
+        n_ent = len(self._fit)
+        cap = max(1, min(int(top_rank_capacity), n_ent + n_cand))  # output slots
+        ref = np.zeros(cap, dtype=np.int64)
+        seq = np.zeros(cap, dtype=np.uint64)
+        n_out = C.c_size_t(0)
+        pad = lambda a: a if a.size else np.zeros(1, dtype=a.dtype)  # noqa: E731
+        e_cols, k_cols = pad(self._cols), pad(c_cols)
+        check(lib.ebic_top_rank_update(
+            self.n_cols, n_ent, ptr(self._off, szp), ptr(e_cols, u16p), ptr(pad(self._fit), f64p),
+            ptr(pad(self._seq), u64p), n_cand, ptr(c_off, szp), ptr(k_cols, u16p), ptr(pad(fit), f64p),
+            float(overlap_threshold), int(top_rank_capacity), C.byref(self._next_seq),
+            ptr(ref, i64p), ptr(seq, u64p), C.byref(n_out)))
+        n = n_out.value
+        ref, seq = ref[:n], seq[:n]
+        # Gather the new list (entries referenced by index, candidates by -(p + 1)).
+        segs, new_fit = [], np.empty(n, dtype=np.float64)
+        for i, r in enumerate(ref.tolist()):
+            if r < 0:
+                p = -r - 1
+                segs.append(c_cols[int(c_off[p]):int(c_off[p + 1])])
+                new_fit[i] = fit[p]
+            else:
+                segs.append(self._cols[int(self._off[r]):int(self._off[r + 1])])
+                new_fit[i] = self._fit[r]
+        new_off = np.zeros(n + 1, dtype=np.uint64)
+        np.cumsum([len(x) for x in segs], out=new_off[1:])
+        new_cols = np.concatenate(segs).astype(np.uint16) if segs else np.zeros(0, dtype=np.uint16)
+        self._off, self._cols, self._fit, self._seq = new_off, new_cols, new_fit, seq.copy()
 
 
 # ---------------------------------------------------------------------------

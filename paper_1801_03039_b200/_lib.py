@@ -17,6 +17,7 @@ u16p = C.POINTER(C.c_uint16)
 u64p = C.POINTER(C.c_uint64)
 f64p = C.POINTER(C.c_double)
 szp = C.POINTER(C.c_size_t)
+i64p = C.POINTER(C.c_int64)
 vp = C.c_void_p
 
 
@@ -61,6 +62,7 @@ SIGNATURES = [
     ("ebic_expand_bicluster", C.c_int, [vp, u16p, C.c_size_t, u64p, u8p, C.c_size_t, C.c_int, C.c_size_t, C.c_double, u64p, u8p, szp]),
     ("ebic_resolve_expand_batch", C.c_int, [vp, szp, u16p, C.c_size_t, C.c_int, C.c_size_t, C.c_double, u64p, u8p, szp]),
     ("ebic_synth_generate", C.c_int, [C.c_size_t, C.c_size_t, C.c_size_t, szp, szp, C.c_int, C.c_size_t, C.c_size_t, C.c_double, C.c_uint64, f64p]),
+    ("ebic_top_rank_update", C.c_int, [C.c_size_t, C.c_size_t, szp, u16p, f64p, u64p, C.c_size_t, szp, u16p, f64p, C.c_double, C.c_size_t, u64p, i64p, u64p, szp]),
 ]
 
 EXPORTED = [s[0] for s in SIGNATURES]

@@ -16,7 +16,7 @@ CSRC = Path(__file__).resolve().parent
 PKG = CSRC.parent
 REPO = PKG.parent
 LIB = PKG / "libebic_b200.so"
-SOURCES = [CSRC / "ebic_b200.cu", CSRC / "synth.cpp"]
+SOURCES = [CSRC / "ebic_b200.cu", CSRC / "synth.cpp", CSRC / "toprank.cpp"]
 DEPS = SOURCES + [CSRC / "kernels.cuh", REPO / "include" / "ebic_b200.h"]
 E2E = PKG / "ebic_e2e_driver"
 E2E_SRC = CSRC / "e2e_driver.cu"

@@ -63,6 +63,18 @@ int guarded(F&& f) {
     }
 }
 
+}  // namespace
+
+namespace ebic_b200_detail {
+// Last-error hook for the host-only translation units (toprank.cpp).
+int set_error(int status, const char* msg) {
+    g_last_error = msg;
+    return status;
+}
+}  // namespace ebic_b200_detail
+
+namespace {
+
 int env_int(const char* name, int dflt) {
     const char* v = std::getenv(name);
     return (v && *v) ? std::atoi(v) : dflt;

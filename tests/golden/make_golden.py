@@ -187,6 +187,74 @@ def fixture_trace(ref: oracle.Ref, name: str) -> None:
     print(f"trace {name}: {len(trace)} batches, {sum(sizes)} series", flush=True)
 
 
+# TopRankList::update sequences: whole populations as the
+# reference GA passes them to the list (elite clones + novel), and the random
+# stress streams with many fitness ties and column collisions.
+TOP_RANK_RUNS = {
+    # name: (rows, cols, blocks, seed, eps, generations, threshold, capacity)
+    "c1": (500, 100, [(50, 10)] * 3, 1, 0.0, 60, 0.75, 100),
+    "c4": (20000, 500, [(600, 20)] * 5, 2026, 1e-9, 12, 0.75, 100),
+}
+
+
+def _stress_updates(seed: int):
+    rng = np.random.default_rng(seed)
+    n_cols = int(rng.integers(6, 140))
+    thr = float(rng.choice([0.75, 0.5, 1.0, 0.25, 0.6]))
+    cap = int(rng.choice([1, 3, 20, 100]))
+    ups = []
+    for _ in range(int(rng.integers(2, 10))):
+        P = int(rng.integers(1, 200))
+        pool = rng.choice(n_cols, size=min(n_cols, int(rng.integers(4, 40))), replace=False)
+        series = [rng.choice(pool, size=min(len(pool), int(rng.integers(2, 10))), replace=False)
+                  for _ in range(P)]
+        off = np.zeros(P + 1, dtype=np.uint64)
+        off[1:] = np.cumsum([len(x) for x in series])
+        fit = rng.integers(-2, 10, size=P).astype(np.float64) * 0.25
+        ups.append((off, np.concatenate(series).astype(np.uint16), fit))
+    return n_cols, thr, cap, ups
+
+
+def fixture_top_rank(ref: oracle.Ref) -> None:
+    streams = []
+    for name, (rows, cols, blocks, seed, eps, gens, thr, cap) in TOP_RANK_RUNS.items():
+        v = ref.generate(rows, cols, blocks, 0, 0, 0, 0.0, seed)
+        m = ref.matrix(v)
+        with tempfile.TemporaryDirectory() as td:
+            path = Path(td) / "pop.bin"
+            ref.run_population_trace(m, path, population=600, iterations=gens - 1, rng_seed=1,
+                                     eps=eps, sigma=0, threads=8)
+            streams.append((name, cols, thr, cap, oracle.read_population_trace(path)))
+    for k in range(24):
+        n_cols, thr, cap, ups = _stress_updates(100 + k)
+        streams.append((f"stress{k}", n_cols, thr, cap, ups))
+    out = {"names": np.array([s[0] for s in streams]),
+           "n_cols": np.array([s[1] for s in streams], dtype=np.uint32),
+           "threshold": np.array([s[2] for s in streams]),
+           "capacity": np.array([s[3] for s in streams], dtype=np.uint32)}
+    for i, (name, n_cols, thr, cap, ups) in enumerate(streams):
+        t = ref.top_rank(n_cols)
+        p_sizes, p_lens, p_cols, p_fit = [], [], [], []
+        e_sizes, e_lens, e_cols, e_fit, e_seq = [], [], [], [], []
+        for off, c, fit in ups:
+            t.update(off, c, fit, thr, cap)
+            eo, ec, ef, es = t.entries()
+            p_sizes.append(len(fit)); p_lens.append(np.diff(off)); p_cols.append(c); p_fit.append(fit)
+            e_sizes.append(len(ef)); e_lens.append(np.diff(eo)); e_cols.append(ec)
+            e_fit.append(ef); e_seq.append(es)
+        out[f"s{i}_pop_sizes"] = np.array(p_sizes, dtype=np.uint32)
+        out[f"s{i}_pop_lens"] = np.concatenate(p_lens).astype(np.uint16)
+        out[f"s{i}_pop_cols"] = np.concatenate(p_cols).astype(np.uint16)
+        out[f"s{i}_pop_fitness"] = np.concatenate(p_fit)
+        out[f"s{i}_top_sizes"] = np.array(e_sizes, dtype=np.uint32)
+        out[f"s{i}_top_lens"] = np.concatenate(e_lens).astype(np.uint16)
+        out[f"s{i}_top_cols"] = np.concatenate(e_cols).astype(np.uint16)
+        out[f"s{i}_top_fitness"] = np.concatenate(e_fit)
+        out[f"s{i}_top_seq"] = np.concatenate(e_seq).astype(np.uint64)
+        print(f"top_rank {name}: {len(ups)} updates, final size {e_sizes[-1]}", flush=True)
+    np.savez_compressed(OUT / "top_rank_updates.npz", **out)
+
+
 def fixture_dropin_json() -> None:
     """Reference `ebic run` output (byte-exact target for the drop-in binary)."""
     args = ["rows=500", "cols=100", "blocks=50x10,50x10,50x10", "seed=1", "population=600",
@@ -208,7 +276,8 @@ def main() -> None:
     jobs = {"acceptance": lambda: fixture_acceptance(ref),
             "trials": lambda: fixture_fitness_trials(ref),
             "expansion": lambda: fixture_expansion(ref),
-            "dropin": fixture_dropin_json}
+            "dropin": fixture_dropin_json,
+            "top_rank": lambda: fixture_top_rank(ref)}
     for t in TRACES:
         jobs[t] = (lambda t=t: fixture_trace(ref, t))
     for name, job in jobs.items():
