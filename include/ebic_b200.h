@@ -71,8 +71,6 @@ typedef struct ebic_ctx_info {
     int layout;           /* last count launch: 0 fp64 tile, 1/2 = exact rank tile (planes),
                              3 = one-plane collapsed rank tile (eps > 0) */
     int consumer_warps;   /* count-kernel consumer warps per CTA */
-    int compact_columns;  /* last count launch staged only its distinct columns
-                             (TMA gather4; stages then depend on the launch) */
 } ebic_ctx_info;
 
 /* Library / device queries. */

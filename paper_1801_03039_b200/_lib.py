@@ -35,7 +35,6 @@ class CtxInfo(C.Structure):
         ("sm_count", C.c_int),
         ("layout", C.c_int),
         ("consumer_warps", C.c_int),
-        ("compact_columns", C.c_int),
     ]
 
 

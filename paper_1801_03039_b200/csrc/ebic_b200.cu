@@ -84,7 +84,7 @@ int env_int(const char* name, int dflt) {
 // context is created so the per-generation launch path makes no getenv calls.
 struct Knobs {
     int force_direct, rpg, rpl, stages, ncw, slice, layout_f64, no_collapse, sched_static,
-        max_parts, reduce_tree, grid, phase_timing, spg, host_copy, compact;
+        max_parts, reduce_tree, grid, phase_timing, spg, host_copy;
     static Knobs from_env() {
         Knobs k;
         k.force_direct = env_int("EBIC_FORCE_DIRECT", 0);
@@ -102,7 +102,6 @@ struct Knobs {
         k.phase_timing = env_int("EBIC_PHASE_TIMING", 0);
         k.spg = env_int("EBIC_SPG", 0);
         k.host_copy = env_int("EBIC_HOST_COPY", 0);
-        k.compact = env_int("EBIC_COMPACT", -1);  // -1 auto, 0 off, 1 force
         return k;
     }
 };
@@ -149,8 +148,6 @@ struct CountConfig {
     int spg = 2;        // rank layout: series per lane group
     int stages = 0;
     uint32_t box_cols = 0, n_boxes = 0, stage_bytes = 0;
-    bool compact = false;  // rank layout: only the launch's columns staged (tile::gather4)
-    uint32_t ring_off = 0, ring_bytes = 0, smem = 0;
 };
 
 struct Tables {
@@ -175,8 +172,6 @@ struct RankLayout {
     CUtensorMap tmap;
     bool tmap_ok = false;
     int tmap_slice = 0;
-    CUtensorMap gmap;  // box {64 elements, 1 column}: TMA gather4 (compact mode)
-    bool gmap_ok = false;
     uint64_t last_use = 0;
 };
 
@@ -416,42 +411,9 @@ CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int
     const size_t budget = (size_t)s.max_smem;
     if (rank_planes) {
         const int want_slice = kn.slice;
-        // Compact column staging with 64-row (128-byte) column slices: used
-        // when all columns of a 128-byte tile do not fit a 3-deep ring (wide
-        // matrices such as C5), or when forced.  Needs one stage of the widest
-        // possible compact tile (every column used) next to the work list.
-        auto try_compact = [&]() -> bool {
-            if (kn.compact == 0 || (want_slice && want_slice != 128) || P > 0xffffffffull) return false;
-            CountConfig c;
-            c.layout = rank_planes;
-            c.slice = 128;
-            c.rpg = 128 / (2 * rank_planes);
-            c.rpl = rank_planes == 2 ? 4 : 8;
-            c.ncw = want_ncw ? (want_ncw == 16 ? 16 : want_ncw == 24 && rank_planes == 1 ? 24 : 32)
-                             : (rank_planes == 1 ? 24 : 32);
-            c.spg = kn.spg == 4 ? 4 : 2;
-            if (c.spg == 4) c.ncw = 16;
-            c.compact = true;
-            // 1 KB stays for static shared memory; 128 B is the window's alignment slack
-            const size_t dyn = budget - 1024;
-            const size_t ro = compact_ring_off((uint32_t)P, (uint32_t)L, (uint32_t)n_cols);
-            if (ro + 128 >= dyn) return false;
-            const size_t ring = dyn - ro - 128;
-            const size_t widest = ((n_cols + 3) / 4 * 4) * 128;
-            if (ring < widest || ring < compact_prologue_bytes((uint32_t)P, (uint32_t)L, (uint32_t)n_cols))
-                return false;
-            c.ring_off = (uint32_t)ro;
-            c.ring_bytes = (uint32_t)ring;
-            c.smem = (uint32_t)dyn;
-            c.stages = 0;
-            best = c;
-            return true;
-        };
-        if (kn.compact == 1 && try_compact()) return best;
         for (int min_stages : {3, 2}) {
             for (int slice : {128, 64}) {
                 if (want_slice && slice != want_slice) continue;
-                if (min_stages == 3 && slice == 64 && try_compact()) return best;
                 CountConfig c;
                 c.layout = rank_planes;
                 c.slice = slice;
@@ -691,23 +653,6 @@ const CUtensorMap& rank_tensor_map(RankLayout& rl, const Shard& s, size_t n_cols
     return rl.tmap;
 }
 
-const CUtensorMap& rank_gather_map(RankLayout& rl, const Shard& s, size_t n_cols) {
-    if (!rl.gmap_ok) {
-        cuuint64_t dims[2] = {(cuuint64_t)(s.ld * rl.planes), (cuuint64_t)n_cols};
-        cuuint64_t strides[1] = {(cuuint64_t)(s.ld * rl.planes * sizeof(uint16_t))};
-        cuuint32_t box[2] = {64, 1};  // one 128-byte column slice per gathered column
-        cuuint32_t estr[2] = {1, 1};
-        CUresult r = tensor_map_encoder()(&rl.gmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, rl.d, dims,
-                                          strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                          CU_TENSOR_MAP_SWIZZLE_NONE,
-                                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) fail(EBIC_ERR_CUDA, "cuTensorMapEncodeTiled (gather) failed (" + std::to_string((int)r) + ")");
-        rl.gmap_ok = true;
-    }
-    return rl.gmap;
-}
-
 // Host-built Eq. 1 tables (same glibc log/exp2 as fitness.hpp:129,131).
 const Tables& ensure_tables(Shard& s, uint64_t sigma, size_t total_rows) {
     Tables& t = s.tables;
@@ -790,11 +735,8 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         p.stage_bytes = c.stage_bytes;
         p.stages = (uint32_t)c.stages;
         p.n_tiles = (uint32_t)((s.rows + c.rpg - 1) / c.rpg);
-        p.scratch_in_stage = (!c.compact && scratch_in_stage(c, P, L)) ? 1u : 0u;
-        p.compact = c.compact ? 1u : 0u;
-        p.ring_off = c.ring_off;
-        p.ring_bytes = c.ring_bytes;
-        const size_t smem = c.compact ? c.smem : tma_smem_bytes(c, P, L);
+        p.scratch_in_stage = scratch_in_stage(c, P, L) ? 1u : 0u;
+        const size_t smem = tma_smem_bytes(c, P, L);
         int grid = std::min<int>((int)p.n_tiles, s.sm_count);
         const int g_env = s.knobs.grid;
         if (g_env > 0) grid = std::min<int>(g_env, (int)p.n_tiles);
@@ -812,9 +754,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         } else {
             p.rank_k = 0x7fff7fffu;
         }
-        const CUtensorMap& tm = c.compact  ? rank_gather_map(*rl, s, ctx.n_cols)
-                                : c.layout ? rank_tensor_map(*rl, s, ctx.n_cols, c)
-                                           : tensor_map(s, ctx.n_cols, c);
+        const CUtensorMap& tm = c.layout ? rank_tensor_map(*rl, s, ctx.n_cols, c) : tensor_map(s, ctx.n_cols, c);
         launch_tma(c, e0, tm, p, grid, smem, st);
     } else {
         const size_t smem = 8 * P + 16;
@@ -1159,7 +1099,6 @@ int ebic_ctx_get_info(const ebic_ctx* ctx, ebic_ctx_info* info) {
         const Shard& s = ctx->shards[0];
         info->rows_per_tile = s.last_cfg.rpg;
         info->stages = s.last_cfg.stages;
-        info->compact_columns = s.last_cfg.compact ? 1 : 0;
         info->grid = s.last_grid;
         info->device_bytes = s.ld * ctx->n_cols * sizeof(double);
         info->sm_count = s.sm_count;

@@ -68,19 +68,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-// TMA tile::gather4 (sm_100a): 4 arbitrary dim-1 indices (columns of the
-// column-major matrix) x box[0] elements starting at dim-0 coordinate c0,
-// written as [4][box0] contiguous elements.
-__device__ __forceinline__ void tma_gather4(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int i0, int i1, int i2, int i3) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(smem_dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(i0), "r"(i1), "r"(i2), "r"(i3),
-        "r"(smem_u32(bar))
-        : "memory");
-}
-
 __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1) {
     asm volatile(
@@ -194,12 +181,6 @@ struct CountParams {
     unsigned int* __restrict__ cbf_ready;
     unsigned int cbf_seq;
     uint64_t table_n;                      // entries of logt/expt (prefetched into L2)
-    // Compact column staging (rank layouts): each tile stages only the columns
-    // the launch uses, gathered 4 at a time by TMA tile::gather4; the ring
-    // depth follows from the number of distinct columns (known in-kernel).
-    uint32_t compact;                      // 1: compact mode
-    uint32_t ring_off;                     // byte offset of the stage ring in shared memory
-    uint32_t ring_bytes;                   // bytes available to the ring
     unsigned long long* __restrict__ phase_ns;  // optional [grid][8] %globaltimer stamps
 };
 
@@ -233,25 +214,6 @@ __host__ __device__ inline size_t count_scratch_bytes(uint32_t P, uint32_t L) {
 }
 __host__ __device__ inline size_t count_meta_bytes(uint32_t P, uint32_t L, bool scratch_in_stage) {
     return count_persist_bytes(P, L) + (scratch_in_stage ? 0 : count_scratch_bytes(P, L) + 16);
-}
-
-// Compact mode shared-memory map:
-//   [full/empty/prologue barriers][work list (persistent)][ucols: compact
-//   position -> column, padded to 4][ring ...]
-// The prologue scratch and the column bitmap (+ per-word prefix) live at the
-// start of the ring: the producer issues its first load only after the
-// prologue has finished.
-__host__ __device__ inline uint32_t compact_words(uint32_t n_cols) { return (n_cols + 31u) / 32u; }
-__host__ __device__ inline size_t compact_ucols_off(uint32_t P, uint32_t L) {
-    const size_t bars = (2 * kMaxStages + 2) * sizeof(uint64_t);
-    return bars + ((count_persist_bytes(P, L) + 15) & ~size_t(15));
-}
-__host__ __device__ inline size_t compact_ring_off(uint32_t P, uint32_t L, uint32_t n_cols) {
-    const size_t off = compact_ucols_off(P, L) + ((2ull * (n_cols + 4) + 15) & ~size_t(15));
-    return (off + 127) & ~size_t(127);
-}
-__host__ __device__ inline size_t compact_prologue_bytes(uint32_t P, uint32_t L, uint32_t n_cols) {
-    return ((count_scratch_bytes(P, L) + 15) & ~size_t(15)) + 8ull * compact_words(n_cols) + 16;
 }
 
 struct WorkList {
@@ -361,27 +323,8 @@ __device__ __forceinline__ void warp_scan64(uint32_t* a, uint32_t* b, int lane) 
 //     on it) -- and copies its columns into its padded list.
 //  E  (only if some series is >= 63 long) list starts of the overflow bucket.
 // Runs while the producer's first TMA stages are in flight.
-// Compact mode (cm.bm != nullptr): the launch's distinct columns get dense
-// positions (ascending column order); pcols then holds position * col_bytes,
-// cm.ucols maps positions back to columns (padded to a multiple of 4 with the
-// last used column) and s_ring receives {U padded, stages, stage bytes, last}.
-struct CompactMap {
-    uint32_t* bm = nullptr;     // [words] column bitmap (scratch)
-    uint32_t* wbase = nullptr;  // [words] exclusive prefix of bitmap popcounts (scratch)
-    uint16_t* ucols = nullptr;  // [U padded] position -> column (persistent)
-    uint32_t* s_ring = nullptr; // {U padded, stages, stage bytes, U}
-};
-
-__device__ __forceinline__ uint32_t compact_pos(const CompactMap& cm, uint32_t c) {
-    const uint32_t wd = c >> 5;
-    return cm.wbase[wd] + __popc(cm.bm[wd] & ((1u << (c & 31u)) - 1u));
-}
-
 __device__ __forceinline__ void build_work_list(const CountParams& p, const WorkList& w, int tid,
-                                                int nthreads, int bar_id, uint32_t col_bytes,
-                                                const CompactMap& cm = CompactMap{}) {
-    const bool compact = cm.bm != nullptr;
-    const uint32_t n_words = compact ? compact_words(p.n_cols) : 0u;
+                                                int nthreads, int bar_id, uint32_t col_bytes) {
     const uint32_t P = p.n_series, L = p.total_len;
     const uint32_t nblk = (P + 31) / 32;
     const int lane = tid & 31, nw = nthreads >> 5;
@@ -416,16 +359,7 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
     }
     for (uint32_t i = tid; i < nblk * kLenBuckets; i += nthreads) w.wh[i] = 0;
     for (int b = tid; b < kLenBuckets; b += nthreads) w.hist[b] = 0;
-    for (uint32_t i = tid; i < n_words; i += nthreads) cm.bm[i] = 0;
     named_bar_sync(bar_id, nthreads);                                        // 1
-
-    if (compact) {  // mark the launch's columns
-        const uint16_t* lc = w.raw + shift;
-        for (uint32_t i = tid; i < L; i += nthreads) {
-            const uint32_t c = lc[i];
-            atomicOr(&cm.bm[c >> 5], 1u << (c & 31u));
-        }
-    }
 
     auto bucket_of = [&](uint32_t s, uint32_t& len) -> uint32_t {
         len = s < P ? w.rel[s + 1] - w.rel[s] : 0u;
@@ -459,48 +393,8 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
             w.wh[blk * kLenBuckets + b] = run;
             run += t;
         }
-    } else if (compact && tid >= 32 + kLenBuckets && tid < 64 + kLenBuckets) {
-        // one warp: exclusive prefix of the bitmap popcounts -> positions
-        const uint32_t ln = tid - (32 + kLenBuckets);
-        const uint32_t seg = (n_words + 31u) / 32u, lo = min(ln * seg, n_words), hi = min(lo + seg, n_words);
-        uint32_t sum = 0;
-        for (uint32_t i = lo; i < hi; ++i) sum += __popc(cm.bm[i]);
-        uint32_t incl = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (ln >= static_cast<uint32_t>(o)) incl += v;
-        }
-        uint32_t run = incl - sum;
-        for (uint32_t i = lo; i < hi; ++i) {
-            cm.wbase[i] = run;
-            run += __popc(cm.bm[i]);
-        }
-        if (ln == 31) {
-            const uint32_t U = incl;
-            const uint32_t upad = U < 4u ? 4u : (U + 3u) & ~3u;
-            const uint32_t sb = upad * col_bytes;
-            uint32_t nst = p.ring_bytes / sb;
-            nst = nst < 1u ? 1u : (nst > static_cast<uint32_t>(kMaxStages) ? kMaxStages : nst);
-            cm.s_ring[0] = upad;
-            cm.s_ring[1] = nst;
-            cm.s_ring[2] = sb;
-            cm.s_ring[3] = U;
-        }
     }
     named_bar_sync(bar_id, nthreads);                                        // 3
-
-    if (compact) {  // position -> column; padding repeats the last used column
-        const uint32_t upad = cm.s_ring[0], U = cm.s_ring[3];
-        for (uint32_t c = tid; c < p.n_cols; c += nthreads) {
-            if (!((cm.bm[c >> 5] >> (c & 31u)) & 1u)) continue;
-            const uint32_t pos = compact_pos(cm, c);
-            cm.ucols[pos] = static_cast<uint16_t>(c);
-            if (pos + 1u == U)
-                for (uint32_t i = U; i < upad; ++i) cm.ucols[i] = static_cast<uint16_t>(c);
-        }
-        if (U == 0u && tid < 4) cm.ucols[tid] = 0;
-    }
 
     const uint32_t lt = (1u << lane) - 1u;
     for (uint32_t blk = tid >> 5; blk < nblk; blk += nw) {
@@ -518,8 +412,7 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
             const uint32_t st = w.hpad[bkt] + r * pad4(len);
             w.sstart[g] = st;
             const uint16_t* from = w.raw + w.rel[s];
-            for (uint32_t i = 0; i < pad4(len); ++i)
-                w.pcols[st + i] = i < len ? (compact ? compact_pos(cm, from[i]) : from[i]) * col_bytes : 0u;
+            for (uint32_t i = 0; i < pad4(len); ++i) w.pcols[st + i] = i < len ? from[i] * col_bytes : 0u;
         }
     }
     named_bar_sync(bar_id, nthreads);                                        // 4
@@ -537,8 +430,7 @@ __device__ __forceinline__ void build_work_list(const CountParams& p, const Work
         for (uint32_t g = ovf + tid; g < P; g += nthreads) {
             const uint32_t len = w.slen[g], st = w.sstart[g];
             const uint16_t* from = w.raw + w.rel[w.sl[g]];
-            for (uint32_t i = 0; i < pad4(len); ++i)
-                w.pcols[st + i] = i < len ? (compact ? compact_pos(cm, from[i]) : from[i]) * col_bytes : 0u;
+            for (uint32_t i = 0; i < pad4(len); ++i) w.pcols[st + i] = i < len ? from[i] * col_bytes : 0u;
         }
         named_bar_sync(bar_id, nthreads);
     }
@@ -1060,32 +952,14 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     // (pointer arithmetic on the shared array keeps LDS addressing).
     unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     const uint32_t P = p.n_series;
-    const bool compact = p.compact != 0;
-    __shared__ uint32_t s_ring[4];  // compact mode: {U padded, stages, stage bytes, U}
-    unsigned char* stage_base;
-    uint64_t* full_bar;
-    unsigned char* scratch;
-    CompactMap cm;
-    if (!compact) {
-        stage_base = smem;
-        full_bar = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * p.stage_bytes);
-    } else {
-        full_bar = reinterpret_cast<uint64_t*>(smem);
-        stage_base = smem + p.ring_off;
-    }
+    unsigned char* stage_base = smem;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + size_t(p.stages) * p.stage_bytes);
     uint64_t* empty_bar = full_bar + kMaxStages;
     uint64_t* prol_bar = empty_bar + kMaxStages;  // work list built (scratch stage released)
     unsigned char* persist = reinterpret_cast<unsigned char*>(prol_bar + 2);
-    if (!compact) {
-        scratch = p.scratch_in_stage ? stage_base + size_t(p.stages - 1) * p.stage_bytes
-                                     : align16(persist, count_persist_bytes(P, p.total_len));
-    } else {
-        scratch = stage_base;  // the ring is idle until the prologue is done
-        cm.ucols = reinterpret_cast<uint16_t*>(smem + compact_ucols_off(P, p.total_len));
-        cm.bm = reinterpret_cast<uint32_t*>(align16(scratch, count_scratch_bytes(P, p.total_len)));
-        cm.wbase = cm.bm + compact_words(p.n_cols);
-        cm.s_ring = s_ring;
-    }
+    unsigned char* scratch = p.scratch_in_stage
+                                 ? stage_base + size_t(p.stages - 1) * p.stage_bytes
+                                 : align16(persist, count_persist_bytes(P, p.total_len));
     const WorkList wl = carve_work_list(persist, scratch, P, p.total_len);
 
     const int warp = threadIdx.x >> 5;
@@ -1094,7 +968,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     if (stamp && threadIdx.x == 0) stamp[0] = global_ns();
 
     if (threadIdx.x == 0) {
-        for (uint32_t s = 0; s < (compact ? static_cast<uint32_t>(kMaxStages) : p.stages); ++s) {
+        for (uint32_t s = 0; s < p.stages; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], NCW);
         }
@@ -1136,32 +1010,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                 }
             }
         }
-        if (compact) {
-            // Column-compact tiles: 4 columns x kDim0PerTile elements per
-            // gather4, spread over the warp's lanes.
-            mbar_wait(prol_bar, 0);
-            const uint32_t ng = s_ring[0] / 4, nst = s_ring[1], sb = s_ring[2];
-            const uint2* uc = reinterpret_cast<const uint2*>(cm.ucols);
-            uint32_t st = 0, phase = 0;
-            for (uint32_t item = blockIdx.x; item < n_items; item += G) {
-                const uint32_t tile = item < full ? item : full + (item - full) / parts;
-                mbar_wait(&empty_bar[st], phase ^ 1u);
-                if (lane == 0) {
-                    s_next[st] = 0;  // published by the arrive below (release)
-                    mbar_arrive_expect_tx(&full_bar[st], sb);
-                }
-                __syncwarp();
-                unsigned char* dst = stage_base + size_t(st) * sb;
-                const int r0 = static_cast<int>(tile * Walker::kDim0PerTile);
-                for (uint32_t g = lane; g < ng; g += 32) {
-                    const uint2 c4 = uc[g];
-                    tma_gather4(dst + size_t(g) * 4 * Walker::kColBytes, &tmap, &full_bar[st], r0,
-                                static_cast<int>(c4.x & 0xffffu), static_cast<int>(c4.x >> 16),
-                                static_cast<int>(c4.y & 0xffffu), static_cast<int>(c4.y >> 16));
-                }
-                if (++st == nst) st = 0, phase ^= 1u;
-            }
-        } else if (lane == 0) {
+        if (lane == 0) {
             uint32_t st = 0, phase = 0, issued = 0;
             for (uint32_t item = blockIdx.x; item < n_items; item += G, ++issued) {
                 const uint32_t tile = item < full ? item : full + (item - full) / parts;
@@ -1181,13 +1030,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     } else {
         // ---------------- consumer warps ----------------
         if (p.host_cbf) stage_host_cbf(p, threadIdx.x, NCW * 32, 1);
-        build_work_list(p, wl, threadIdx.x, NCW * 32, 1, Walker::kColBytes, cm);
+        build_work_list(p, wl, threadIdx.x, NCW * 32, 1, Walker::kColBytes);
         if (threadIdx.x == 0) mbar_arrive(prol_bar);
-        // Ring geometry: kernel parameters, or (compact mode) shared memory,
-        // read where used so no register stays live across the walk.
-        volatile uint32_t* ring_geom = s_ring;
-        auto nstages = [&]() { return p.compact ? ring_geom[1] : p.stages; };
-        auto sbytes = [&]() { return p.compact ? ring_geom[2] : p.stage_bytes; };
         if (stamp && threadIdx.x == 0) stamp[1] = global_ns();
 
         // Rows excluded from the layout (collapsed rank layout: two values
@@ -1202,14 +1046,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                 const uint32_t len = wl.slen[g];
                 const uint32_t* pc = wl.pcols + wl.sstart[g];
                 bool ok = true;
-                auto col_of = [&](uint32_t off) -> uint32_t {
-                    const uint32_t q = off / Walker::kColBytes;
-                    return compact ? cm.ucols[q] : q;
-                };
                 if (len > 1) {
-                    double prev = __ldg(rowv + col_of(pc[0]));
+                    double prev = __ldg(rowv + pc[0] / Walker::kColBytes);
                     for (uint32_t k = 1; k < len; ++k) {
-                        const double cur = __ldg(rowv + col_of(pc[k]));
+                        const double cur = __ldg(rowv + pc[k] / Walker::kColBytes);
                         ok = ok & step_ok<false>(prev, cur, p.eps);
                         prev = cur;
                     }
@@ -1239,7 +1079,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             unsigned long long excl_word = 0ull;
             if (p.row_excl) excl_word = __ldg(p.row_excl + (r0 >> 6));
             mbar_wait(&full_bar[st], phase);
-            const unsigned char* base = stage_base + size_t(st) * sbytes() + gl * Walker::kLaneBytes;
+            const unsigned char* base = stage_base + size_t(st) * p.stage_bytes + gl * Walker::kLaneBytes;
             if (p.row_excl) excl = static_cast<uint32_t>(excl_word >> (r0 & 63)) & ((1u << RPL) - 1u);
             // rows of this tile that exist (the last tile may be partial)
             const typename Walker::Mask vmask = Walker::valid(r0, p.n_rows, excl, p.rank_k);
@@ -1287,7 +1127,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty_bar[st]);
-            if (++st == nstages()) st = 0, phase ^= 1u;
+            if (++st == p.stages) st = 0, phase ^= 1u;
         }
     }
     __syncthreads();

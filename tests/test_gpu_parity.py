@@ -27,10 +27,6 @@ KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NCW="24"), dict(EBIC_N
                   [dict(EBIC_LAYOUT_F64="1", EBIC_RPG=str(g), EBIC_RPL=str(l))
                    for g in (32, 16, 8, 4) for l in (1, 2)] +
                   [dict(EBIC_LAYOUT_F64="1", EBIC_NCW="16"), dict(EBIC_FORCE_DIRECT="1")])
-# Column-compact staging (TMA gather4 of the launch's distinct columns), forced
-# on widths where the full tile would fit anyway.
-COMPACT_CONFIGS = [dict(EBIC_COMPACT="1"), dict(EBIC_COMPACT="1", EBIC_NO_COLLAPSE="1"),
-                   dict(EBIC_COMPACT="1", EBIC_SPG="4"), dict(EBIC_COMPACT="1", EBIC_NCW="16")]
 
 
 @contextmanager
@@ -103,8 +99,7 @@ def test_trace_golden(name):
             assert bits_equal(f, fit)
 
 
-@pytest.mark.parametrize("cfg", KERNEL_CONFIGS + COMPACT_CONFIGS,
-                         ids=lambda d: "-".join(f"{k}={v}" for k, v in d.items()) or "default")
+@pytest.mark.parametrize("cfg", KERNEL_CONFIGS, ids=lambda d: "-".join(f"{k}={v}" for k, v in d.items()) or "default")
 @pytest.mark.parametrize("name", ["c1", "c1e", "c3", "c4"])
 def test_every_kernel_config_on_traces(cfg, name):
     t = trace(name)
@@ -118,8 +113,7 @@ def test_every_kernel_config_on_traces(cfg, name):
                 assert bits_equal(f, fit)
 
 
-@pytest.mark.parametrize("cfg", KERNEL_CONFIGS[:8] + KERNEL_CONFIGS[10:11] + KERNEL_CONFIGS[-1:] + COMPACT_CONFIGS,
-                         ids=str)
+@pytest.mark.parametrize("cfg", KERNEL_CONFIGS[:8] + KERNEL_CONFIGS[10:11] + KERNEL_CONFIGS[-1:], ids=str)
 def test_edge_cases_vs_oracle(cfg):
     """Ragged row counts, ties, +-0, NaN/inf cells, odd eps values, len-1 series."""
     rng = np.random.default_rng(7)
@@ -291,9 +285,8 @@ def test_finalize_biclusters_c4_top_series():
         assert b.rows == wr and [int(f) for f in b.row_flags] == wf
 
 
-@pytest.mark.parametrize("compact", ["0", "1"])
 @pytest.mark.parametrize("n_dirty", [0, 1, 7, 40, 3000])
-def test_collapsed_rank_layout_with_dirty_rows(n_dirty, compact):
+def test_collapsed_rank_layout_with_dirty_rows(n_dirty):
     """eps > 0 with clean rows uses the one-plane collapsed layout (<= test);
     rows holding two values closer than eps (or NaN) cannot be represented and
     are evaluated exactly in fp64 by the kernel.  Too many of them: two planes."""
@@ -309,7 +302,7 @@ def test_collapsed_rank_layout_with_dirty_rows(n_dirty, compact):
             v[r, b] = v[r, a] + eps * [0.5, 1.0, 0.999, 0.25][k % 4]  # inside (v_a, v_a + eps]
     series = random_population(rng, n_cols, 700)
     pop = cbf(series)
-    with env(EBIC_COMPACT=compact), eb.Evaluator(v) as ev:
+    with eb.Evaluator(v) as ev:
         for e in (eps, 2 * eps, 1e-9):
             got = ev.count_matches(pop, e)
             want = port.count_matches(v, pop.offsets, pop.col_indices, e)
@@ -319,30 +312,3 @@ def test_collapsed_rank_layout_with_dirty_rows(n_dirty, compact):
             assert bits_equal(f, wf)
         info = ev.info()
     assert info.layout == (3 if n_dirty <= 64 else 2)
-
-
-@pytest.mark.parametrize("n_cols,used,compact", [(1200, 1200, 1), (1200, 500, 1), (1200, 3, 1),
-                                                  (900, 900, 1), (1500, 700, None), (2048, 1600, None)])
-def test_compact_columns_on_wide_matrices(n_cols, used, compact):
-    """Widths whose full 64-row tile does not fit a 3-deep ring stage only the
-    launch's distinct columns (gather4) when a one-stage ring of every column
-    fits; every column used = one-stage ring.  Wider: 32-row tiles."""
-    rng = np.random.default_rng(n_cols + used)
-    rows = 3000
-    v = np.round(rng.standard_normal((rows, n_cols)), 2)
-    pool = rng.choice(n_cols, size=used, replace=False)
-    series = [list(rng.choice(pool, size=min(used, int(rng.integers(2, 9))), replace=False))
-              for _ in range(600)]
-    cover = list(pool)  # make sure every pool column appears
-    for i in range(0, len(cover) - 1, 8):
-        series.append(cover[i:i + 8] if len(cover[i:i + 8]) >= 2 else cover[i - 1:i + 1])
-    series = series[:2048]
-    pop = cbf(series)
-    with eb.Evaluator(v) as ev:
-        for e in (0.0, 1e-9, 0.05):
-            got = ev.count_matches(pop, e)
-            want = port.count_matches(v, pop.offsets, pop.col_indices, e)
-            assert (got == want).all(), e
-        info = ev.info()
-    if compact is not None:
-        assert info.compact_columns == compact
