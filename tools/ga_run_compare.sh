@@ -15,7 +15,7 @@ run_pair() {  # name, args...
   ./oracle/_ref/ebic_dropin_run "$@" threads=$T out=/tmp/ga_dropin_$name.json 2>> $out
   if cmp -s /tmp/ga_ref_$name.json /tmp/ga_dropin_$name.json; then echo "json identical" >> $out; else echo "JSON DIFFERS" >> $out; fi
 }
+# BASELINE.json configs 0 and 3 at their stated iteration counts.
 run_pair c1 rows=500 cols=100 blocks=50x10,50x10,50x10 seed=1 population=600 iterations=1000 rng_seed=42 epsilon=1e-9 overlap_threshold=0.5 threshold=none
-run_pair c3 rows=5000 cols=200 blocks=200x20,200x20,200x20,200x20,200x20 overlap=5 seed=5 population=600 iterations=300 rng_seed=7 epsilon=1e-9
-run_pair c4 rows=20000 cols=500 blocks=600x20,600x20,600x20,600x20,600x20 seed=2026 population=600 iterations=100 rng_seed=1 epsilon=1e-9
+run_pair c4 rows=20000 cols=500 blocks=600x20,600x20,600x20,600x20,600x20 seed=2026 population=600 iterations=5000 rng_seed=1 epsilon=1e-9
 cat $out
