@@ -5,8 +5,8 @@
  * seam: its evolutionary loop calls inline free functions.  Each entry point
  * below replaces one of those functions (cited as reference file:line, paths
  * relative to /root/reference/proj/include/ebic/).  The repo's shadowing
- * headers include/ebic/fitness.hpp and include/ebic/expansion.hpp bind these
- * entry points behind the reference's own C++ signatures.
+ * headers include/ebic/{fitness,expansion,evolution}.hpp bind these entry
+ * points behind the reference's own C++ signatures.
  *
  * Conventions
  *  - Plain pointers and sizes only; no C++ or torch types cross the ABI.
