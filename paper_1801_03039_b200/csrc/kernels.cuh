@@ -731,18 +731,22 @@ struct RankWalker {
     static constexpr int kSeriesPerGroup = SPG;               // independent walks per group
     static constexpr int kFieldBits = 32 / SPG;               // packed per-series counts
     static_assert(SPG == 2 || SPG == 4, "2 or 4 series per lane group");
+    // Result bits: bit 15 / 31 of ok word k hold the lane's rows 2k / 2k+1.
+    // tally() folds word k down by k bits (rows land on bits 15-k / 31-k)
+    // and counts once; `m` is the lane's valid-row mask in that folded form.
     struct Mask {
-        uint32_t m[kWords];
+        uint32_t m;  // folded valid-row mask
         uint32_t k;  // per-pair constant: 0x7fff7fff (strict <) or 0x80008000 (<=, collapsed)
     };
     // excl: bit j set = the lane's row j is excluded (fixed up separately).
     __device__ __forceinline__ static Mask valid(uint32_t row0, uint32_t n_rows, uint32_t excl,
                                                  uint32_t kconst) {
         Mask v;
+        v.m = 0;
 #pragma unroll
         for (int k = 0; k < kWords; ++k)
-            v.m[k] = ((row0 + 2 * k < n_rows && !((excl >> (2 * k)) & 1u)) ? 0x8000u : 0u) |
-                     ((row0 + 2 * k + 1 < n_rows && !((excl >> (2 * k + 1)) & 1u)) ? 0x80000000u : 0u);
+            v.m |= (((row0 + 2 * k < n_rows && !((excl >> (2 * k)) & 1u)) ? 0x8000u : 0u) |
+                    ((row0 + 2 * k + 1 < n_rows && !((excl >> (2 * k + 1)) & 1u)) ? 0x80000000u : 0u)) >> k;
         v.k = PLANES == 2 ? 0x7fff7fffu : kconst;
         return v;
     }
@@ -783,10 +787,11 @@ struct RankWalker {
         }
     }
     __device__ __forceinline__ static uint32_t tally(const uint32_t* ok, const Mask& vm) {
-        uint32_t c = 0;
+        constexpr uint32_t kRes = 0x80008000u;  // result bits of an ok word
+        uint32_t f = ok[0] & kRes;
 #pragma unroll
-        for (int k = 0; k < kWords; ++k) c += __popc(ok[k] & vm.m[k]);
-        return c;
+        for (int k = 1; k < kWords; ++k) f |= (ok[k] & kRes) >> k;
+        return __popc(f & vm.m);
     }
     // Two series of exactly L columns, walked interleaved (independent chains).
     template <int L>
