@@ -92,8 +92,15 @@ int main(int argc, char** argv) {
         return 2;
     }
     ebic_ctx* ctx = nullptr;
-    int dev = 0;
-    if (ebic_ctx_create(values.data(), rows, cols, &dev, 1, &ctx) != EBIC_OK) {
+    std::vector<int> devs;  // EBIC_GPUS="0,1,..." as in include/ebic/fitness.hpp (default 0)
+    if (const char* e = std::getenv("EBIC_GPUS"))
+        for (const char* q = e; *q;) {
+            devs.push_back(std::atoi(q));
+            while (*q && *q != ',') ++q;
+            if (*q == ',') ++q;
+        }
+    if (devs.empty()) devs.push_back(0);
+    if (ebic_ctx_create(values.data(), rows, cols, devs.data(), (int)devs.size(), &ctx) != EBIC_OK) {
         std::fprintf(stderr, "ctx: %s\n", ebic_last_error());
         return 2;
     }

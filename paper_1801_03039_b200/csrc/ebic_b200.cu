@@ -84,7 +84,7 @@ int env_int(const char* name, int dflt) {
 // context is created so the per-generation launch path makes no getenv calls.
 struct Knobs {
     int force_direct, rpg, rpl, stages, ncw, slice, layout_f64, no_collapse, sched_static,
-        max_parts, reduce_tree, grid, phase_timing, spg, host_copy;
+        max_parts, reduce_tree, grid, phase_timing, spg, host_copy, xshard;
     static Knobs from_env() {
         Knobs k;
         k.force_direct = env_int("EBIC_FORCE_DIRECT", 0);
@@ -102,6 +102,7 @@ struct Knobs {
         k.phase_timing = env_int("EBIC_PHASE_TIMING", 0);
         k.spg = env_int("EBIC_SPG", 0);
         k.host_copy = env_int("EBIC_HOST_COPY", 0);
+        k.xshard = env_int("EBIC_XSHARD", 1);  // in-kernel cross-shard reduction
         return k;
     }
 };
@@ -241,7 +242,8 @@ void grow_mapped(unsigned char** p, size_t* cap, size_t need) {
     *p = nullptr;
     size_t n = std::max(need, *cap * 2);
     n = (n + 255) & ~size_t(255);
-    CK(cudaHostAlloc(reinterpret_cast<void**>(p), n, cudaHostAllocMapped));
+    // portable: with several shards, any device's final CTA may write results
+    CK(cudaHostAlloc(reinterpret_cast<void**>(p), n, cudaHostAllocMapped | cudaHostAllocPortable));
     std::memset(*p, 0, n);
     *cap = n;
 }
@@ -287,6 +289,12 @@ struct ebic_ctx {
     size_t row_begin = 0;   // global row of shards[0]
     size_t total_rows = 0;  // rows of the full matrix (fitness tables, sigma)
     std::vector<Shard> shards;
+    // Cross-shard reduction state (several shards): per-series accumulator and
+    // ticket on shards[0]'s device, reachable from every shard's device.
+    int xshard = -1;  // -1 not set up, 0 unavailable, 1 ready
+    unsigned long long* d_xacc = nullptr;
+    size_t xacc_cap = 0;
+    unsigned int* d_xticket = nullptr;
 };
 
 namespace {
@@ -683,7 +691,8 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
                   size_t L, double eps, uint64_t* d_counts, double* d_fit, uint64_t sigma,
                   cudaStream_t st, uint64_t cols_base, unsigned long long* done_flag = nullptr,
                   unsigned long long done_seq = 0, const void* host_cbf = nullptr,
-                  size_t cbf_bytes = 0) {
+                  size_t cbf_bytes = 0, unsigned long long* xacc = nullptr,
+                  unsigned int* xticket = nullptr, uint32_t n_xshards = 0) {
     if (P == 0) return;
     if (P > 0xffffffffull || L > 0xffffffffull || s.rows > 0xffffffffull)
         fail(EBIC_ERR_INVALID_ARGUMENT, "population or shard too large for one launch");
@@ -707,6 +716,9 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
     p.reduce_striped = s.knobs.reduce_tree ? 0u : 1u;
     p.done_flag = done_flag;
     p.done_seq = done_seq;
+    p.xacc = xacc;
+    p.xticket = xticket;
+    p.n_xshards = n_xshards;
     if (host_cbf) {
         p.host_cbf = static_cast<const uint4*>(host_cbf);
         p.dev_cbf = reinterpret_cast<uint4*>(s.d_in);
@@ -825,6 +837,106 @@ inline double us_since(HostClock::time_point& t) {
     return d;
 }
 
+// Cross-shard reduction setup: peer access from every shard's device to
+// shards[0]'s, and the accumulator (zeroed; the last arriver of each launch
+// re-zeroes what it consumes).  Returns false when unavailable.
+bool setup_xshard(ebic_ctx& ctx, size_t P) {
+    if (ctx.xshard == 0 || !ctx.shards[0].knobs.xshard) return false;
+    const int home = ctx.shards[0].device;
+    if (ctx.xshard < 0) {
+        for (const Shard& s : ctx.shards) {
+            if (s.device == home) continue;
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, s.device, home) != cudaSuccess || !can) {
+                (void)cudaGetLastError();
+                ctx.xshard = 0;
+                return false;
+            }
+            DeviceGuard g(s.device);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(home, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                (void)cudaGetLastError();
+                ctx.xshard = 0;
+                return false;
+            }
+            (void)cudaGetLastError();
+        }
+        DeviceGuard g(home);
+        CK(cudaMalloc(&ctx.d_xticket, sizeof(unsigned int)));
+        CK(cudaMemset(ctx.d_xticket, 0, sizeof(unsigned int)));
+        ctx.xshard = 1;
+    }
+    if (P > ctx.xacc_cap) {
+        DeviceGuard g(home);
+        for (const Shard& s : ctx.shards) CK(cudaStreamSynchronize(s.stream));
+        if (ctx.d_xacc) CK(cudaFree(ctx.d_xacc));
+        ctx.d_xacc = nullptr;
+        const size_t n = std::max<size_t>(P, 2 * ctx.xacc_cap);
+        CK(cudaMalloc(&ctx.d_xacc, n * sizeof(unsigned long long)));
+        CK(cudaMemset(ctx.d_xacc, 0, n * sizeof(unsigned long long)));
+        ctx.xacc_cap = n;
+    }
+    return true;
+}
+
+// Several shards, one launch each: every shard's kernel adds its totals into
+// the home accumulator; the last one to finish writes counts + fitness for
+// the whole matrix into shards[0]'s mapped buffer and raises its flag.
+void host_evaluate_xshard(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_t P, size_t L,
+                          double eps, bool want_fit, uint64_t sigma, uint64_t* counts_out,
+                          double* fit_out, HostClock::time_point& tp) {
+    Shard& s0 = ctx.shards[0];
+    const size_t off_bytes = (P + 1) * sizeof(uint64_t);
+    const size_t cols_at = (off_bytes + 15) & ~size_t(15);
+    const size_t in_bytes = cols_at + L * sizeof(uint16_t);
+    {
+        DeviceGuard g(s0.device);
+        grow_mapped(&s0.h_map, &s0.h_map_cap, 128 + P * 16);
+    }
+    uint64_t* m_counts = reinterpret_cast<uint64_t*>(s0.h_map + 128);
+    double* m_fit = want_fit ? reinterpret_cast<double*>(s0.h_map + 128 + P * 8) : nullptr;
+    const unsigned long long seq = ++s0.seq;
+    for (Shard& s : ctx.shards) {
+        DeviceGuard g(s.device);
+        grow_mapped(&s.h_in_map, &s.h_in_map_cap, in_bytes + 64);
+        grow_device(&s.d_in, &s.d_in_cap, in_bytes + 64);
+        std::memcpy(s.h_in_map, off, off_bytes);
+        if (L) std::memcpy(s.h_in_map + cols_at, cols, L * sizeof(uint16_t));
+        if (s.knobs.host_copy)
+            CK(cudaMemcpyAsync(s.d_in, s.h_in_map, in_bytes, cudaMemcpyHostToDevice, s.stream));
+        if (&s == &s0) s0.host_us[1] += us_since(tp);
+        const auto* d_off = reinterpret_cast<const uint64_t*>(s.d_in);
+        const auto* d_cols = reinterpret_cast<const uint16_t*>(s.d_in + cols_at);
+        launch_count(ctx, s, d_off, d_cols, P, L, eps, m_counts, m_fit, sigma, s.stream, 0,
+                     reinterpret_cast<unsigned long long*>(s0.h_map), seq,
+                     s.knobs.host_copy ? nullptr : s.h_in_map, in_bytes, ctx.d_xacc, ctx.d_xticket,
+                     static_cast<uint32_t>(ctx.shards.size()));
+        if (&s == &s0) s0.host_us[2] += us_since(tp);
+    }
+    volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(s0.h_map);
+    for (uint64_t spin = 0;; ++spin) {
+        if (*flag == seq) break;
+        if ((spin & 1023) == 1023) {
+            bool idle = true;
+            for (Shard& s : ctx.shards) {
+                DeviceGuard g(s.device);
+                const cudaError_t e = cudaStreamQuery(s.stream);
+                if (e == cudaErrorNotReady) idle = false;
+                else if (e != cudaSuccess) cuda_check(e, "count kernel");
+            }
+            if (idle) {
+                if (*flag == seq) break;
+                fail(EBIC_ERR_CUDA, "cross-shard count finished without its completion flag");
+            }
+        }
+    }
+    s0.host_us[3] += us_since(tp);
+    if (counts_out) std::memcpy(counts_out, m_counts, P * 8);
+    if (want_fit) std::memcpy(fit_out, m_fit, P * 8);
+    s0.host_us[4] += us_since(tp);
+    ++s0.host_calls;
+}
+
 void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_t P, double eps,
                    bool want_fit, uint64_t sigma, uint64_t* counts_out, double* fit_out) {
     if (P == 0) return;
@@ -837,6 +949,10 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
     const size_t cols_at = (off_bytes + 15) & ~size_t(15);
     const size_t in_bytes = cols_at + L * sizeof(uint16_t);
     const bool single = ctx.shards.size() == 1;
+    if (!single && P <= kMaxSeriesPerLaunch && L <= kMaxLenPerLaunch && setup_xshard(ctx, P)) {
+        host_evaluate_xshard(ctx, off, cols, P, L, eps, want_fit, sigma, counts_out, fit_out, tp);
+        return;
+    }
     for (Shard& s : ctx.shards) {
         DeviceGuard g(s.device);
         grow_mapped(&s.h_in_map, &s.h_in_map_cap, in_bytes + 64);
@@ -1083,6 +1199,11 @@ int ebic_ctx_destroy(ebic_ctx* ctx) {
     return guarded([&] {
         if (!ctx) return;
         for (Shard& s : ctx->shards) free_shard(s);
+        if (ctx->d_xacc || ctx->d_xticket) {
+            cudaSetDevice(ctx->shards[0].device);
+            cudaFree(ctx->d_xacc);
+            cudaFree(ctx->d_xticket);
+        }
         delete ctx;
     });
 }

@@ -181,6 +181,14 @@ struct CountParams {
     unsigned int* __restrict__ cbf_ready;
     unsigned int cbf_seq;
     uint64_t table_n;                      // entries of logt/expt (prefetched into L2)
+    // Cross-shard reduction (one process, several row shards / devices): the
+    // final CTA of every shard's launch adds its per-series totals into
+    // xacc (home device memory, peer-accessible) and takes a system-scope
+    // ticket; the last shard to arrive writes counts + fitness for the whole
+    // matrix and raises the done flag.  No launch waits for another.
+    unsigned long long* __restrict__ xacc;  // [P] or nullptr (single shard)
+    unsigned int* __restrict__ xticket;
+    uint32_t n_xshards;
     unsigned long long* __restrict__ phase_ns;  // optional [grid][8] %globaltimer stamps
 };
 
@@ -486,6 +494,32 @@ __device__ __forceinline__ void signal_done(const CountParams& p) {
     }
 }
 
+// Final CTA of one shard, after adding its totals into p.xacc: the system-
+// scope ticket orders every shard's additions before the last arriver's
+// reads; that CTA takes each total (and re-zeroes it) with one exchange,
+// writes counts + Eq. 1 and signals completion.  The others just return.
+__device__ __forceinline__ void cross_shard_finish(const CountParams& p) {
+    __shared__ int s_xlast;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        s_xlast = atomicAdd_system(p.xticket, 1u) == p.n_xshards - 1;
+        __threadfence_system();
+    }
+    __syncthreads();
+    if (!s_xlast) return;
+    const uint32_t P = p.n_series;
+    for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
+        const uint64_t c = atomicExch_system(p.xacc + s, 0ull);
+        p.counts_out[s] = c;
+        if (p.fitness_out)
+            p.fitness_out[s] = fitness_from_tables(c, p.offsets[s + 1] - p.offsets[s], p.sigma,
+                                                   p.logt, p.expt);
+    }
+    if (threadIdx.x == 0) atomicExch_system(p.xticket, 0u);
+    signal_done(p);
+}
+
 __device__ __forceinline__ void count_epilogue_striped(const CountParams& p, const uint32_t* s_cnt,
                                                        const uint32_t* slot_series) {
     const uint32_t P = p.n_series;
@@ -505,6 +539,19 @@ __device__ __forceinline__ void count_epilogue_striped(const CountParams& p, con
     if (stamp && threadIdx.x == 0) stamp[5] = global_ns();
     if (!s_last) return;
     if (stamp && threadIdx.x == 0) stamp[7] = global_ns();
+    if (p.xacc) {
+        for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
+            uint4* a = reinterpret_cast<uint4*>(acc + size_t(s) * kStripes);
+            const uint4 x = __ldcg(a), y = __ldcg(a + 1);
+            const uint64_t c = uint64_t(x.x) + x.y + x.z + x.w + y.x + y.y + y.z + y.w;
+            a[0] = make_uint4(0, 0, 0, 0);
+            a[1] = make_uint4(0, 0, 0, 0);
+            if (c) atomicAdd_system(p.xacc + s, static_cast<unsigned long long>(c));
+        }
+        if (threadIdx.x == 0) p.done[kMaxGroups] = 0u;
+        cross_shard_finish(p);
+        return;
+    }
     for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
         uint4* a = reinterpret_cast<uint4*>(acc + size_t(s) * kStripes);
         const uint4 x = __ldcg(a), y = __ldcg(a + 1);
@@ -559,6 +606,15 @@ __device__ __forceinline__ void count_epilogue(const CountParams& p, const uint3
     if (stamp && threadIdx.x == 0) stamp[7] = global_ns();
 
     // last group reducer: final counts + fused Eq. 1
+    if (p.xacc) {
+        for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
+            const uint64_t c = sum_rows(grows, P, s, 0, n_groups);
+            if (c) atomicAdd_system(p.xacc + s, static_cast<unsigned long long>(c));
+        }
+        if (threadIdx.x == 0) p.done[kMaxGroups] = 0u;
+        cross_shard_finish(p);
+        return;
+    }
     for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
         const uint64_t c = sum_rows(grows, P, s, 0, n_groups);
         p.counts_out[s] = c;

@@ -169,16 +169,24 @@ def test_wide_matrix_direct_path():
     assert (got == port.count_matches(v, pop.offsets, pop.col_indices, 0.05)).all()
 
 
-def test_row_shards_on_one_device_are_partition_invariant():
-    """devices=[0,0,0]: three 64-row-aligned shards on one GPU, exact host reduction."""
-    t = trace("c3")
+@pytest.mark.parametrize("xshard", ["1", "0"])
+@pytest.mark.parametrize("devices,name", [([0, 0, 0], "c3"), ([0, 0], "c4"), ([0] * 5, "c1e")])
+def test_row_shards_on_one_device_are_partition_invariant(xshard, devices, name):
+    """Several 64-row-aligned shards on one GPU.  EBIC_XSHARD=1: every shard's
+    kernel adds its totals into one accumulator and the last to finish writes
+    counts + fitness (no launch waits for another, so the shards may run in any
+    order); EBIC_XSHARD=0: exact host reduction."""
+    t = trace(name)
     v = t.matrix()
-    with eb.Evaluator(v, devices=[0, 0, 0]) as ev:
-        assert ev.info().n_shards == 3
-        for off, cols, counts, fit in t.batches[:4]:
-            f, c = ev.evaluate_population(eb.CbfPopulation(off, cols), eb.FitnessParams(t.sigma),
-                                          t.eps, return_counts=True)
-            assert (c == counts).all() and bits_equal(f, fit)
+    with env(EBIC_XSHARD=xshard), eb.Evaluator(v, devices=devices) as ev:
+        assert ev.info().n_shards >= 2  # 64-row aligned: fewer shards than devices on small matrices
+        for rep in range(2):
+            for off, cols, counts, fit in t.batches[:4]:
+                f, c = ev.evaluate_population(eb.CbfPopulation(off, cols), eb.FitnessParams(t.sigma),
+                                              t.eps, return_counts=True)
+                assert (c == counts).all() and bits_equal(f, fit)
+                c2 = ev.count_matches(eb.CbfPopulation(off, cols), t.eps)
+                assert (c2 == counts).all()
 
 
 def test_shard_contexts_sum_to_whole():
