@@ -10,6 +10,7 @@
 // glibc libm calls, so matrices are bit-identical to ebic::generate for the same
 // ScenarioSpec (pinned by tests/test_synth.py against oracle/_ref).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -17,6 +18,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ebic_b200.h"
@@ -55,6 +57,80 @@ class SynthRng {
         spare_ = radius * std::sin(angle);
         have_spare_ = true;
         return mean + sd * radius * std::cos(angle);
+    }
+
+    // m[i] = normal(0, 1) for i < n, in order -- the bulk of generate()'s draws
+    // (the background of every cell).  Same values as the sequential loop:
+    // the pairs' raw engine outputs are drawn in order (into m itself, two
+    // slots per pair), then every pair's Box-Muller transform -- the same glibc
+    // log/sqrt/sin/cos in the same expression order -- runs on all host
+    // threads.  A rejected u1 (engine output < 2^11, p = 2^-53) switches the
+    // rest to the sequential loop at exactly that point.
+    void fill_standard_normals(double* m, size_t n) {
+        size_t i = 0;
+        if (n && have_spare_) m[i++] = normal(0.0, 1.0);
+        const size_t pairs = (n - i) / 2;
+        if (pairs < (size_t{1} << 16)) {
+            for (; i < n; ++i) m[i] = normal(0.0, 1.0);
+            return;
+        }
+        uint64_t* raw = reinterpret_cast<uint64_t*>(m + i);
+        // Pipeline: this thread draws pairs in order and publishes how many
+        // are ready; workers transform blocks as soon as they are drawn.
+        constexpr size_t kBlock = size_t{1} << 14;
+        std::atomic<size_t> drawn{0}, next{0}, limit{pairs};
+        std::atomic<bool> done{false};
+        const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+        const double* const out0 = m + i;
+        auto transform = [&] {
+            for (;;) {
+                const size_t b = next.fetch_add(kBlock);
+                size_t e = std::min(b + kBlock, pairs);
+                if (b >= pairs) return;
+                for (;;) {  // wait until the block is drawn (or drawing stopped short)
+                    const size_t lim = limit.load(std::memory_order_acquire);
+                    e = std::min(e, lim);
+                    if (b >= e) return;
+                    if (drawn.load(std::memory_order_acquire) >= e) break;
+                    if (done.load(std::memory_order_acquire) && drawn.load(std::memory_order_acquire) < e) {
+                        e = std::min(e, drawn.load(std::memory_order_acquire));
+                        break;
+                    }
+                    std::this_thread::yield();
+                }
+                double* out = const_cast<double*>(out0);
+                for (size_t k = b; k < e; ++k) {
+                    const double u1 = static_cast<double>(raw[2 * k] >> 11) * 0x1.0p-53;
+                    const double u2 = static_cast<double>(raw[2 * k + 1] >> 11) * 0x1.0p-53;
+                    const double radius = std::sqrt(-2.0 * std::log(u1));
+                    const double angle = 2.0 * kPi * u2;
+                    const double spare = radius * std::sin(angle);
+                    out[2 * k] = 0.0 + 1.0 * radius * std::cos(angle);
+                    out[2 * k + 1] = 0.0 + 1.0 * spare;
+                }
+            }
+        };
+        std::vector<std::thread> pool;
+        for (unsigned t = 0; t + 1 < nt; ++t) pool.emplace_back(transform);
+        size_t good = pairs;  // pairs whose u1 needs no redraw
+        for (size_t k = 0; k < pairs; ++k) {
+            const uint64_t a = eng_();
+            if ((a >> 11) == 0) {  // normal() would redraw u1 here: finish sequentially
+                good = k;
+                limit.store(k, std::memory_order_release);
+                break;
+            }
+            raw[2 * k] = a;
+            raw[2 * k + 1] = eng_();
+            if (((k + 1) & (kBlock - 1)) == 0) drawn.store(k + 1, std::memory_order_release);
+        }
+        drawn.store(good, std::memory_order_release);
+        done.store(true, std::memory_order_release);
+        transform();  // this thread helps with what is left
+        for (std::thread& th : pool) th.join();
+        // The rest in order: the odd tail, or everything from a rejected u1 on
+        // (that draw is consumed; normal()'s do-while continues with the next).
+        for (i += 2 * good; i < n; ++i) m[i] = normal(0.0, 1.0);
     }
 
   private:
@@ -142,7 +218,7 @@ extern "C" int ebic_synth_generate(size_t n_rows, size_t n_cols, size_t n_blocks
         }
 
         double* m = values_out;
-        for (size_t i = 0; i < n_rows * n_cols; ++i) m[i] = rng.normal(0.0, 1.0);
+        rng.fill_standard_normals(m, n_rows * n_cols);
 
         if (pattern == kTrend) {
             std::vector<size_t> row_cols;

@@ -141,6 +141,22 @@ def test_synth_generate_matches_reference_generator():
             assert (a.view(np.uint64) == b.view(np.uint64)).all()
 
 
+@pytest.mark.parametrize("pat", range(6))
+def test_synth_generate_bulk_path_matches_reference(pat):
+    """Matrices above 2^17 cells take the multi-threaded background fill
+    (raw engine draws in order, Box-Muller pairs in parallel); odd cell counts
+    and a spare normal left by the pattern draws (odd column / row counts)
+    exercise its edges."""
+    ref = oracle.Ref()
+    for (rows, cols) in [(1001, 263), (700, 401), (640, 512)]:
+        blocks = [(40, 9), (35, 7)]
+        noise = 0.3 if pat % 2 else 0.0
+        spec = eb.ScenarioSpec(rows, cols, blocks, eb.Pattern(pat), 2, 2, noise, 7 + pat)
+        a = eb.synth_generate(spec).values
+        b = ref.generate(rows, cols, blocks, pat, 2, 2, noise, 7 + pat)
+        assert (a.view(np.uint64) == b.view(np.uint64)).all(), (rows, cols)
+
+
 def test_synth_generate_errors():
     with pytest.raises(ValueError):
         eb.synth_generate(eb.ScenarioSpec(0, 10, [], eb.Pattern(0)))
