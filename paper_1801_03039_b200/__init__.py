@@ -539,13 +539,14 @@ class TopRankList:
     def best_fitness(self) -> float:  # :151
         return float(self._fit[0]) if len(self._fit) else 0.0
 
-    @property
-    def entries(self) -> List[TopRankEntry]:
+    def entries(self) -> List[TopRankEntry]:  # :148
         return [TopRankEntry([int(c) for c in self._cols[int(self._off[i]):int(self._off[i + 1])]],
                              float(self._fit[i]), int(self._seq[i])) for i in range(len(self._fit))]
 
     @staticmethod
-    def overlap(a: Sequence[int], b: Sequence[int]) -> float:  # :154-160
+    def overlap(a, b) -> float:  # :154-160 (TopRankEntry or plain series)
+        a = a.series if hasattr(a, "series") else a
+        b = b.series if hasattr(b, "series") else b
         return len(set(int(x) for x in a) & set(int(x) for x in b)) / min(len(a), len(b))
 
     def update(self, population, fitness, overlap_threshold: float = 0.75,

@@ -800,12 +800,16 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
 void validate_cbf(const size_t* off, const uint16_t* cols, size_t P, size_t n_cols) {
     if (!off) fail(EBIC_ERR_INVALID_ARGUMENT, "corrupt CBF");
     if (off[0] != 0) fail(EBIC_ERR_RUNTIME, "corrupt CBF");
-    for (size_t p = 0; p < P; ++p)
-        if (off[p + 1] < off[p]) fail(EBIC_ERR_RUNTIME, "corrupt CBF");
+    // Branch-free reductions (vectorised by the compiler); the error paths
+    // are taken only after the scan.
+    size_t descending = 0;
+    for (size_t p = 0; p < P; ++p) descending |= static_cast<size_t>(off[p + 1] < off[p]);
+    if (descending) fail(EBIC_ERR_RUNTIME, "corrupt CBF");
     const size_t L = off[P];
     if (L && !cols) fail(EBIC_ERR_INVALID_ARGUMENT, "corrupt CBF");
-    for (size_t i = 0; i < L; ++i)
-        if (cols[i] >= n_cols) fail(EBIC_ERR_INVALID_ARGUMENT, "invalid series");
+    uint16_t hi = 0;
+    for (size_t i = 0; i < L; ++i) hi = std::max(hi, cols[i]);
+    if (L && hi >= n_cols) fail(EBIC_ERR_INVALID_ARGUMENT, "invalid series");
 }
 
 // Packs the CBF into pinned memory, copies it to every shard, launches the

@@ -127,11 +127,12 @@ def test_series_list_input_and_entries_view():
     top = TopRankList(10)
     top.update([[0, 1, 2], [0, 1, 3], [5, 6], [7, 8]], [3.0, 2.0, 2.0, -1.0], 0.5, 100)
     # [0,1,3] overlaps [0,1,2] by 2/3 > 0.5 and has lower fitness: blocked.
-    assert [(e.series, e.fitness, e.seq) for e in top.entries] == [([0, 1, 2], 3.0, 0),
+    assert [(e.series, e.fitness, e.seq) for e in top.entries()] == [([0, 1, 2], 3.0, 0),
                                                                   ([5, 6], 2.0, 1)]
     top.update([[0, 1, 4, 5]], [4.0], 0.5, 100)  # evicts [0,1,2] (2/3 > 0.5), keeps [5,6] (1/2)
-    assert [(e.series, e.seq) for e in top.entries] == [([0, 1, 4, 5], 2), ([5, 6], 1)]
+    assert [(e.series, e.seq) for e in top.entries()] == [([0, 1, 4, 5], 2), ([5, 6], 1)]
     assert TopRankList.overlap([0, 1, 4, 5], [5, 6]) == 0.5
+    assert TopRankList.overlap(top.entries()[0], top.entries()[1]) == 0.5
     assert len(top) == 2 and not top.empty() and top.best_fitness() == 4.0
 
 
