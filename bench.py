@@ -431,7 +431,6 @@ def run_ours(args):
 
     phases = None
     if os.environ.get("EBIC_PHASE_TIMING"):
-        n = C_size_t = None
         import ctypes as C
         stamps = np.zeros((4096, 8), dtype=np.uint64)
         nc = C.c_size_t(0)
