@@ -206,6 +206,39 @@ int ebic_synth_generate(size_t n_rows, size_t n_cols, size_t n_blocks, const siz
                         const size_t* block_cols, int pattern, size_t overlap_rows,
                         size_t overlap_cols, double noise_sd, uint64_t seed, double* values_out);
 
+/* ---- multi-process row shards: reduction inside the count kernels -------- */
+
+/* One process per GPU, each holding a shard context (ebic_ctx_create_shard),
+ * replaces count_matches' row-chunk partial sums (fitness.hpp:100-118) across
+ * processes without a separate collective: every rank's count kernel adds its
+ * shard's per-series totals into one accumulator on rank 0's GPU (CUDA IPC
+ * peer memory, system-scope atomics) and takes a ticket; the last rank's
+ * kernel writes the whole-matrix counts and Eq. 1 fitness into a POSIX
+ * shared-memory block every rank has mapped, then raises its flag.  No
+ * kernel waits for another (ranks may share a GPU).
+ *   rank 0:     ebic_xgroup_create(ctx0, max_series, "/name", handle)
+ *   broadcast:  handle (EBIC_XGROUP_HANDLE_BYTES) and the name to all ranks
+ *   every rank: ebic_xgroup_join(ctx, handle, "/name", n_ranks, max_series, &g)
+ *   per call (same increasing seq on every rank):
+ *               ebic_xgroup_evaluate(g, offsets, cols, P, sigma, eps, seq, counts, fitness)
+ *           or  ebic_xgroup_count(g, d_off, d_cols, P, L, eps, sigma, want_fit, seq, stream)
+ *               + ebic_xgroup_wait(g, seq, P, counts, fitness)
+ *   teardown:   ebic_xgroup_destroy on every rank (rank 0 last: it owns the memory). */
+#define EBIC_XGROUP_HANDLE_BYTES 64
+typedef struct ebic_xgroup ebic_xgroup;
+int ebic_xgroup_create(ebic_ctx* ctx, size_t max_series, const char* shm_name, void* handle_out);
+int ebic_xgroup_join(ebic_ctx* ctx, const void* handle, const char* shm_name, int n_ranks,
+                     size_t max_series, ebic_xgroup** group_out);
+int ebic_xgroup_evaluate(ebic_xgroup* g, const size_t* offsets, const uint16_t* cols, size_t n_series,
+                         uint64_t sigma, double eps, uint64_t seq, uint64_t* counts_out,
+                         double* fitness_out);
+int ebic_xgroup_count(ebic_xgroup* g, const uint64_t* d_offsets, const uint16_t* d_cols,
+                      size_t n_series, size_t total_len, double eps, uint64_t sigma, int want_fitness,
+                      uint64_t seq, void* stream);
+int ebic_xgroup_wait(ebic_xgroup* g, uint64_t seq, size_t n_series, uint64_t* counts_out,
+                     double* fitness_out);
+int ebic_xgroup_destroy(ebic_xgroup* g);
+
 /* ---- top-rank admission (evolution.hpp:168-206) ------------------------- */
 
 /* Replaces TopRankList::update (evolution.hpp:168-206), host only, stateless.

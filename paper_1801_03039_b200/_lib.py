@@ -62,6 +62,12 @@ SIGNATURES = [
     ("ebic_expand_bicluster", C.c_int, [vp, u16p, C.c_size_t, u64p, u8p, C.c_size_t, C.c_int, C.c_size_t, C.c_double, u64p, u8p, szp]),
     ("ebic_resolve_expand_batch", C.c_int, [vp, szp, u16p, C.c_size_t, C.c_int, C.c_size_t, C.c_double, u64p, u8p, szp]),
     ("ebic_synth_generate", C.c_int, [C.c_size_t, C.c_size_t, C.c_size_t, szp, szp, C.c_int, C.c_size_t, C.c_size_t, C.c_double, C.c_uint64, f64p]),
+    ("ebic_xgroup_create", C.c_int, [vp, C.c_size_t, C.c_char_p, vp]),
+    ("ebic_xgroup_join", C.c_int, [vp, vp, C.c_char_p, C.c_int, C.c_size_t, C.POINTER(vp)]),
+    ("ebic_xgroup_evaluate", C.c_int, [vp, szp, u16p, C.c_size_t, C.c_uint64, C.c_double, C.c_uint64, u64p, f64p]),
+    ("ebic_xgroup_count", C.c_int, [vp, vp, vp, C.c_size_t, C.c_size_t, C.c_double, C.c_uint64, C.c_int, C.c_uint64, vp]),
+    ("ebic_xgroup_wait", C.c_int, [vp, C.c_uint64, C.c_size_t, u64p, f64p]),
+    ("ebic_xgroup_destroy", C.c_int, [vp]),
     ("ebic_top_rank_update", C.c_int, [C.c_size_t, C.c_size_t, szp, u16p, f64p, u64p, C.c_size_t, szp, u16p, f64p, C.c_double, C.c_size_t, u64p, i64p, u64p, szp]),
 ]
 

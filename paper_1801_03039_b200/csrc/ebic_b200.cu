@@ -8,6 +8,9 @@
 // Row chunks become per-device row shards held column-major in HBM; one kernel
 // launch evaluates a whole generation against a shard.
 #include <cuda.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
@@ -19,6 +22,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
+#include <atomic>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -1151,6 +1157,68 @@ void for_each_bit(const uint64_t* bits, size_t words, F&& f) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Multi-process row shards (one process per GPU): the count kernels reduce
+// across processes themselves.  Rank 0 owns one device allocation
+// [ticket | 256 B pad | accumulator u64[max_series]] shared through a CUDA IPC
+// handle, and a POSIX shared-memory result block [flag (128 B) | counts |
+// fitness] that every rank maps and registers with its CUDA context.  Each
+// rank's final CTA adds its shard's totals into the accumulator and takes the
+// ticket; the last rank's final CTA writes counts + Eq. 1 for the whole matrix
+// into the shared block and raises its flag, which every rank's host polls.
+// No kernel ever waits for another, so ranks may even share one GPU.
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr size_t kXAccOffset = 256;
+
+// Rank 0's accumulator between ebic_xgroup_create and its own join.
+std::mutex& xgroup_owned_mu() {
+    static std::mutex m;
+    return m;
+}
+std::map<std::string, unsigned char*>& xgroup_owned() {
+    static std::map<std::string, unsigned char*> t;
+    return t;
+}
+
+}  // namespace
+
+struct ebic_xgroup {
+    ebic_ctx* ctx = nullptr;
+    int n_ranks = 0;
+    bool owner = false;          // rank 0: allocated the accumulator, unlinks the shm
+    size_t max_series = 0;
+    unsigned char* d_base = nullptr;  // accumulator allocation (own or IPC-opened)
+    unsigned char* shm = nullptr;     // mapped result block
+    size_t shm_bytes = 0;
+    std::string shm_name;
+    unsigned long long last_seq = 0;
+};
+
+namespace {
+
+size_t xgroup_shm_bytes(size_t max_series) {
+    const size_t b = 128 + 16 * max_series;
+    return (b + 4095) & ~size_t(4095);
+}
+
+unsigned char* map_shm(const char* name, size_t bytes, bool create) {
+    const int fd = shm_open(name, create ? (O_CREAT | O_RDWR | O_EXCL) : O_RDWR, 0600);
+    if (fd < 0) fail(EBIC_ERR_RUNTIME, std::string("shm_open failed for ") + name);
+    if (create && ftruncate(fd, static_cast<off_t>(bytes)) != 0) {
+        close(fd);
+        fail(EBIC_ERR_RUNTIME, "ftruncate of the shared result block failed");
+    }
+    void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) fail(EBIC_ERR_RUNTIME, "mmap of the shared result block failed");
+    if (create) std::memset(p, 0, bytes);
+    return static_cast<unsigned char*>(p);
+}
+
+}  // namespace
+
 // ===========================================================================
 // C ABI
 // ===========================================================================
@@ -1286,7 +1354,7 @@ int ebic_count_matches_device(ebic_ctx* ctx, const uint64_t* d_offsets, const ui
         const bool whole = ctx->row_begin == 0 && ctx->n_rows == ctx->total_rows;
         if (d_fitness_out && !whole) fail(EBIC_ERR_INVALID_ARGUMENT, "fitness needs reduced counts on a shard context");
         if (n_series > kMaxSeriesPerLaunch || total_len > kMaxLenPerLaunch)
-            fail(EBIC_ERR_INVALID_ARGUMENT, "device batch exceeds 4096 series / 16384 columns; split it");
+            fail(EBIC_ERR_INVALID_ARGUMENT, "device batch exceeds 2048 series / 8192 columns; split it");
         cudaStream_t st = static_cast<cudaStream_t>(stream);  // 0 = legacy default stream
         launch_count(*ctx, s, d_offsets, d_cols, n_series, total_len, eps, d_counts_out, d_fitness_out,
                      sigma, st, 0);  // device CBF: offsets[0] == 0 (cbf.hpp:43-52)
@@ -1436,6 +1504,190 @@ int ebic_resolve_expand_batch(ebic_ctx* ctx, const size_t* offsets, const uint16
             }
             row_counts[s] = n - start;
         }
+    });
+}
+
+
+// ---- multi-process row shards: in-kernel reduction over peer memory --------
+
+int ebic_xgroup_create(ebic_ctx* ctx, size_t max_series, const char* shm_name, void* handle_out) {
+    return guarded([&] {
+        Shard& s = single_shard(ctx);
+        if (!shm_name || !handle_out || max_series == 0) fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(s.device);
+        unsigned char* d = nullptr;
+        CK(cudaMalloc(&d, kXAccOffset + max_series * sizeof(unsigned long long)));
+        CK(cudaMemset(d, 0, kXAccOffset + max_series * sizeof(unsigned long long)));
+        cudaIpcMemHandle_t h;
+        const cudaError_t e = cudaIpcGetMemHandle(&h, d);
+        if (e != cudaSuccess) {
+            cudaFree(d);
+            cuda_check(e, "cudaIpcGetMemHandle");
+        }
+        unsigned char* shm = nullptr;
+        try {
+            shm = map_shm(shm_name, xgroup_shm_bytes(max_series), true);
+        } catch (...) {
+            cudaFree(d);
+            throw;
+        }
+        munmap(shm, xgroup_shm_bytes(max_series));  // each rank (rank 0 too) maps it in join
+        // Stash the allocation for rank 0's join: the handle's first bytes are
+        // opaque; keep the pointer in a process-local table keyed by the name.
+        std::memcpy(handle_out, &h, sizeof h);
+        static_assert(sizeof(cudaIpcMemHandle_t) <= EBIC_XGROUP_HANDLE_BYTES, "handle size");
+        std::lock_guard<std::mutex> lock(xgroup_owned_mu());
+        xgroup_owned()[shm_name] = d;
+    });
+}
+
+int ebic_xgroup_join(ebic_ctx* ctx, const void* handle, const char* shm_name, int n_ranks,
+                     size_t max_series, ebic_xgroup** group_out) {
+    return guarded([&] {
+        Shard& s = single_shard(ctx);
+        if (!handle || !shm_name || !group_out || n_ranks < 1 || max_series == 0)
+            fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard g(s.device);
+        auto grp = std::make_unique<ebic_xgroup>();
+        grp->ctx = ctx;
+        grp->n_ranks = n_ranks;
+        grp->max_series = max_series;
+        grp->shm_name = shm_name;
+        {
+            std::lock_guard<std::mutex> lock(xgroup_owned_mu());
+            auto it = xgroup_owned().find(shm_name);
+            if (it != xgroup_owned().end()) {
+                grp->owner = true;
+                grp->d_base = it->second;
+                xgroup_owned().erase(it);
+            }
+        }
+        if (!grp->owner) {
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, handle, sizeof h);
+            void* p = nullptr;
+            CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+            grp->d_base = static_cast<unsigned char*>(p);
+        }
+        grp->shm_bytes = xgroup_shm_bytes(max_series);
+        grp->shm = map_shm(shm_name, grp->shm_bytes, false);
+        const cudaError_t e = cudaHostRegister(grp->shm, grp->shm_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+        if (e != cudaSuccess) {
+            munmap(grp->shm, grp->shm_bytes);
+            if (!grp->owner) cudaIpcCloseMemHandle(grp->d_base);
+            else cudaFree(grp->d_base);
+            cuda_check(e, "cudaHostRegister of the shared result block");
+        }
+        grp->last_seq = *reinterpret_cast<volatile unsigned long long*>(grp->shm);
+        *group_out = grp.release();
+    });
+}
+
+namespace {
+
+void xgroup_launch(ebic_xgroup* g, const uint64_t* d_off, const uint16_t* d_cols, size_t P, size_t L,
+                   double eps, uint64_t sigma, bool want_fit, uint64_t seq, cudaStream_t st,
+                   const void* host_cbf, size_t cbf_bytes) {
+    ebic_ctx& ctx = *g->ctx;
+    Shard& s = ctx.shards[0];
+    if (P > g->max_series) fail(EBIC_ERR_INVALID_ARGUMENT, "population larger than the group's max_series");
+    if (P > kMaxSeriesPerLaunch || L > kMaxLenPerLaunch)
+        fail(EBIC_ERR_INVALID_ARGUMENT, "batch exceeds 2048 series / 8192 columns; split it");
+    unsigned char* dev_shm = nullptr;
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev_shm), g->shm, 0));
+    auto* counts = reinterpret_cast<uint64_t*>(dev_shm + 128);
+    auto* fit = want_fit ? reinterpret_cast<double*>(dev_shm + 128 + 8 * g->max_series) : nullptr;
+    auto* ticket = reinterpret_cast<unsigned int*>(g->d_base);
+    auto* acc = reinterpret_cast<unsigned long long*>(g->d_base + kXAccOffset);
+    launch_count(ctx, s, d_off, d_cols, P, L, eps, counts, fit, sigma, st, 0,
+                 reinterpret_cast<unsigned long long*>(dev_shm), seq, host_cbf, cbf_bytes, acc, ticket,
+                 static_cast<uint32_t>(g->n_ranks));
+}
+
+void xgroup_wait(ebic_xgroup* g, uint64_t seq, size_t P, uint64_t* counts_out, double* fit_out,
+                 cudaStream_t st) {
+    volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(g->shm);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (uint64_t spin = 0;; ++spin) {
+        if (*flag >= seq) break;
+        if ((spin & 4095) == 4095) {
+            const cudaError_t e = cudaStreamQuery(st);
+            if (e != cudaSuccess && e != cudaErrorNotReady) cuda_check(e, "count kernel");
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(60))
+                fail(EBIC_ERR_RUNTIME, "cross-rank reduction timed out (did every rank launch this call?)");
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    if (counts_out) std::memcpy(counts_out, g->shm + 128, P * 8);
+    if (fit_out) std::memcpy(fit_out, g->shm + 128 + 8 * g->max_series, P * 8);
+    g->last_seq = seq;
+}
+
+}  // namespace
+
+int ebic_xgroup_count(ebic_xgroup* g, const uint64_t* d_offsets, const uint16_t* d_cols, size_t n_series,
+                      size_t total_len, double eps, uint64_t sigma, int want_fitness, uint64_t seq,
+                      void* stream) {
+    return guarded([&] {
+        if (!g) fail(EBIC_ERR_INVALID_ARGUMENT, "null group");
+        if (seq <= g->last_seq) fail(EBIC_ERR_INVALID_ARGUMENT, "call numbers must increase");
+        if (n_series == 0) return;
+        if (!d_offsets) fail(EBIC_ERR_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(g->ctx->shards[0].device);
+        xgroup_launch(g, d_offsets, d_cols, n_series, total_len, eps, sigma, want_fitness != 0, seq,
+                      static_cast<cudaStream_t>(stream), nullptr, 0);
+    });
+}
+
+int ebic_xgroup_wait(ebic_xgroup* g, uint64_t seq, size_t n_series, uint64_t* counts_out,
+                     double* fitness_out) {
+    return guarded([&] {
+        if (!g) fail(EBIC_ERR_INVALID_ARGUMENT, "null group");
+        if (n_series > g->max_series) fail(EBIC_ERR_INVALID_ARGUMENT, "n_series above max_series");
+        xgroup_wait(g, seq, n_series, counts_out, fitness_out, g->ctx->shards[0].stream);
+    });
+}
+
+int ebic_xgroup_evaluate(ebic_xgroup* g, const size_t* offsets, const uint16_t* cols, size_t n_series,
+                         uint64_t sigma, double eps, uint64_t seq, uint64_t* counts_out,
+                         double* fitness_out) {
+    return guarded([&] {
+        if (!g) fail(EBIC_ERR_INVALID_ARGUMENT, "null group");
+        if (seq <= g->last_seq) fail(EBIC_ERR_INVALID_ARGUMENT, "call numbers must increase");
+        if (n_series == 0) return;
+        ebic_ctx& ctx = *g->ctx;
+        Shard& s = ctx.shards[0];
+        validate_cbf(offsets, cols, n_series, ctx.n_cols);
+        const size_t L = offsets[n_series];
+        DeviceGuard dg(s.device);
+        const size_t off_bytes = (n_series + 1) * sizeof(uint64_t);
+        const size_t cols_at = (off_bytes + 15) & ~size_t(15);
+        const size_t in_bytes = cols_at + L * sizeof(uint16_t);
+        grow_mapped(&s.h_in_map, &s.h_in_map_cap, in_bytes + 64);
+        grow_device(&s.d_in, &s.d_in_cap, in_bytes + 64);
+        std::memcpy(s.h_in_map, offsets, off_bytes);
+        if (L) std::memcpy(s.h_in_map + cols_at, cols, L * sizeof(uint16_t));
+        xgroup_launch(g, reinterpret_cast<const uint64_t*>(s.d_in),
+                      reinterpret_cast<const uint16_t*>(s.d_in + cols_at), n_series, L, eps, sigma,
+                      fitness_out != nullptr, seq, s.stream, s.h_in_map, in_bytes);
+        xgroup_wait(g, seq, n_series, counts_out, fitness_out, s.stream);
+    });
+}
+
+int ebic_xgroup_destroy(ebic_xgroup* g) {
+    return guarded([&] {
+        if (!g) return;
+        DeviceGuard dg(g->ctx->shards[0].device);
+        cudaStreamSynchronize(g->ctx->shards[0].stream);
+        cudaHostUnregister(g->shm);
+        munmap(g->shm, g->shm_bytes);
+        if (g->owner) {
+            cudaFree(g->d_base);
+            shm_unlink(g->shm_name.c_str());
+        } else {
+            cudaIpcCloseMemHandle(g->d_base);
+        }
+        delete g;
     });
 }
 
