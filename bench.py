@@ -24,8 +24,13 @@ Arms
                      unmodified headers compiled here) on all host threads.
 
 Multi-GPU (torchrun, one process per GPU): rows are sharded (64-row aligned);
-each rank counts its shard, counts are all-reduced (NCCL, int64 sum), then the
-Eq. 1 kernel runs on the reduced counts.  Time = max over ranks.
+each rank counts its shard.  `e2e` (host buffers, the public C ABI) sums
+across ranks inside the count kernels: every rank's final CTA adds into rank
+0's accumulator through CUDA IPC peer memory and the last one writes counts +
+Eq. 1 into a shared-memory block all ranks read.  `value` (inputs resident in
+HBM, steps pipelined) all-reduces the counts with NCCL and runs the Eq. 1
+kernel on them (--reduce collective, default), or uses the in-kernel sum
+with a host wait per step (--reduce kernel).  Time = max over ranks.
 """
 from __future__ import annotations
 
@@ -203,7 +208,11 @@ def workload_config(t, args):
             "rows": s["rows"], "cols": s["cols"],
             "series_per_step": round(float(np.mean([len(b[0]) - 1 for b in t.batches])), 1),
             "eps": t.eps, "sigma": t.sigma, "l2": "evicted between timed steps (512 MB read, outside the timed events)",
-            "parallelism": f"rows sharded over {args.gpus} GPU(s)"}
+            "parallelism": f"rows sharded over {args.gpus} GPU(s)"
+                           + ("" if args.gpus == 1 and not args.force_sharded else
+                              ("; value: cross-rank sum inside the count kernels (CUDA IPC peer memory)"
+                               if args.reduce == "kernel" else "; value: NCCL all-reduce of counts")
+                              + "; e2e: cross-rank sum inside the count kernels")}
 
 
 # ---------------------------------------------------------------------------
@@ -306,14 +315,17 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     sharded = world > 1 or args.force_sharded
     if sharded:
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
-        dist.init_process_group("nccl", rank=rank, world_size=world,
-                                device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", rank=rank, world_size=world,
+                                    device_id=torch.device("cuda", local))
+        else:  # several ranks on one GPU (tests of the kernel-side reduction)
+            dist.init_process_group("gloo", rank=rank, world_size=world)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
 
@@ -340,6 +352,8 @@ def run_ours(args):
             cols=torch.from_numpy(cols.view(np.int16)).to(dev),
             counts=torch.zeros(len(off) - 1, dtype=torch.int64, device=dev),
             fit=torch.zeros(len(off) - 1, dtype=torch.float64, device=dev),
+            h_counts=np.zeros(len(off) - 1, dtype=np.uint64),
+            h_fit=np.zeros(len(off) - 1, dtype=np.float64),
             want=(counts, fit)))
     # L2 eviction between timed steps by READING 512 MB (4x L2): leaves L2 full
     # of clean lines, so the timed kernel does not pay for write-backs that a
@@ -350,8 +364,37 @@ def run_ours(args):
     def evict_l2():
         torch.sum(flush, dim=0, keepdim=True, out=flush_sink)
 
+    # Cross-rank reduction inside the count kernels (ebic_xgroup_*): set up
+    # once, torch.distributed only broadcasts the IPC handle.  The host path
+    # (e2e) always uses it; the device-resident path (`value`) uses it with
+    # --reduce kernel, else an NCCL all-reduce that pipelines without host syncs.
+    import ctypes as C
+    xgroup = None
+    if sharded:
+        import uuid
+        handle = (C.c_ubyte * 64)()
+        name = f"/ebic_bench_{os.getpid()}_{uuid.uuid4().hex[:8]}"
+        if rank == 0:
+            _lib.check(_lib.lib.ebic_xgroup_create(ev.handle, 2048, name.encode(), handle))
+        obj = [bytes(handle), name]
+        dist.broadcast_object_list(obj, src=0)
+        xgroup = _lib.vp()
+        _lib.check(_lib.lib.ebic_xgroup_join(ev.handle, (C.c_ubyte * 64).from_buffer_copy(obj[0]),
+                                             obj[1].encode(), world, 2048, C.byref(xgroup)))
+        dist.barrier()
+    xg = xgroup if args.reduce == "kernel" else None
+    xseq = [0]
+
     def step(b):
-        if sharded:
+        if xg is not None:
+            xseq[0] += 1
+            _lib.check(_lib.lib.ebic_xgroup_count(
+                xg, b["off"].data_ptr(), b["cols"].data_ptr(), b["P"], b["L"], t.eps, t.sigma, 1,
+                xseq[0], st))
+            _lib.check(_lib.lib.ebic_xgroup_wait(
+                xg, xseq[0], b["P"], b["h_counts"].ctypes.data_as(_lib.u64p),
+                b["h_fit"].ctypes.data_as(_lib.f64p)))
+        elif sharded:
             _lib.check(_lib.lib.ebic_count_matches_device(
                 ev.handle, b["off"].data_ptr(), b["cols"].data_ptr(), b["P"], b["L"], t.eps,
                 t.sigma, b["counts"].data_ptr(), None, st))
@@ -364,7 +407,7 @@ def run_ours(args):
                 ev.handle, b["off"].data_ptr(), b["cols"].data_ptr(), b["P"], b["L"], t.eps,
                 t.sigma, b["counts"].data_ptr(), b["fit"].data_ptr(), st))
 
-    launches_per_step = 2 if sharded else 1
+    launches_per_step = 2 if (sharded and xg is None) else 1
 
     # warm-up + correctness gate on every batch (bit-exact vs the reference trace)
     for k in range(max(args.warmup, len(dev_batches))):
@@ -377,8 +420,11 @@ def run_ours(args):
     for b in dev_batches:
         step(b)
         torch.cuda.synchronize()
-        c = b["counts"].cpu().numpy().astype(np.uint64)
-        f = b["fit"].cpu().numpy()
+        if xg is not None:
+            c, f = b["h_counts"].copy(), b["h_fit"].copy()
+        else:
+            c = b["counts"].cpu().numpy().astype(np.uint64)
+            f = b["fit"].cpu().numpy()
         assert (c == b["want"][0]).all(), "count mismatch vs reference"
         assert (f.view(np.uint64) == b["want"][1].view(np.uint64)).all(), "fitness mismatch"
 
@@ -411,7 +457,8 @@ def run_ours(args):
     total_ms = float(sum(times))
     clk = clocks.stop() if rank == 0 else None
     if sharded:
-        tt = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([total_ms], dtype=torch.float64,
+                          device=dev if args.backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
     value = series / (total_ms / 1e3)
@@ -485,6 +532,49 @@ def run_ours(args):
         h2d //= args.steps
         d2h //= args.steps
 
+    # ---- e2e at N ranks: the host path through the in-kernel cross-rank sum
+    # (ebic_xgroup_evaluate: host CBF staged in-kernel, every rank's count,
+    # the last rank's kernel writes counts + fitness to shared host memory) ----
+    e2e_sh = None
+    if sharded:
+        n_sh = 0
+        el = 0.0
+        host_pops = [(np.ascontiguousarray(off, dtype=np.uint64), np.ascontiguousarray(cols, dtype=np.uint16))
+                     for off, cols, _, _ in t.batches]
+        hc = np.zeros(2048, dtype=np.uint64)
+        hf = np.zeros(2048, dtype=np.float64)
+
+        def call(off, cols):
+            xseq[0] += 1
+            _lib.check(_lib.lib.ebic_xgroup_evaluate(
+                xgroup, off.ctypes.data_as(_lib.szp), cols.ctypes.data_as(_lib.u16p), len(off) - 1,
+                t.sigma, t.eps, xseq[0], hc.ctypes.data_as(_lib.u64p), hf.ctypes.data_as(_lib.f64p)))
+        for k in range(max(3, args.warmup)):
+            call(*host_pops[k % len(host_pops)])
+        for k in range(args.steps):
+            off, cols = host_pops[k % len(host_pops)]
+            evict_l2()
+            torch.cuda.synchronize()
+            dist.barrier()  # every rank enters the call together (outside the timing)
+            a = time.perf_counter()
+            call(off, cols)
+            el += time.perf_counter() - a
+            n_sh += len(off) - 1
+            want = t.batches[k % len(t.batches)]
+            assert (hf[:len(off) - 1].view(np.uint64) == want[3].view(np.uint64)).all(), "e2e fitness mismatch"
+        tt = torch.tensor([el], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+        pb = [len(off) - 1 for off, _ in host_pops]
+        lb = [int(off[-1]) for off, _ in host_pops]
+        nb = len(host_pops)
+        e2e_sh = {"value": n_sh / el, "unit": UNIT,
+                  "h2d_bytes_per_step": int(sum((p + 1) * 8 + l * 2 for p, l in zip(pb, lb)) / nb),
+                  "d2h_bytes_per_step": int(sum(16 * p for p in pb) / nb),
+                  "us_per_step": el / args.steps * 1e6,
+                  "caller": "ebic_xgroup_evaluate (C ABI) on every rank, host buffers; "
+                            "cross-rank sum inside the count kernels"}
+
     big = None
     if not sharded and not args.no_large:
         ev.close()
@@ -518,7 +608,7 @@ def run_ours(args):
             "data": "synthetic (reference generator, bit-identical) + reference GA batches",
             "config": workload_config(t, args),
             "roofline": roof, "cpu_baseline": cb, "clocks": clk,
-            "e2e": ({"value": e2e_cpp["e2e_biclusters_per_s"], "unit": UNIT,
+            "e2e": e2e_sh if sharded else ({"value": e2e_cpp["e2e_biclusters_per_s"], "unit": UNIT,
                      "h2d_bytes_per_step": e2e_cpp["h2d_bytes_per_step"],
                      "d2h_bytes_per_step": e2e_cpp["d2h_bytes_per_step"],
                      "us_per_step": e2e_cpp["us_per_step"],
@@ -540,6 +630,12 @@ def run_ours(args):
             "diag_back_to_back_us_per_step": b2b_us,
         }
         print(json.dumps(line), flush=True)
+    if xgroup is not None:
+        if rank != 0:
+            _lib.check(_lib.lib.ebic_xgroup_destroy(xgroup))
+        dist.barrier()
+        if rank == 0:
+            _lib.check(_lib.lib.ebic_xgroup_destroy(xgroup))
     ev.close()
     if sharded:
         dist.destroy_process_group()
@@ -555,6 +651,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-large", action="store_true",
                     help="skip the config-5 (200,000 x 1000) roofline run")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="torch.distributed backend (gloo: several ranks sharing one GPU, "
+                         "kernel-side reduction only)")
+    ap.add_argument("--reduce", choices=["kernel", "collective"], default="collective",
+                    help="device-resident multi-process path (`value`): cross-rank sum in the count "
+                         "kernels, or NCCL (default: pipelines without host syncs); the e2e host "
+                         "path always sums inside the kernels")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the multi-process shard path (all-reduce + fitness kernel) even at N=1")
     ap.add_argument("--cpu-budget", type=float, default=15.0,

@@ -1191,6 +1191,7 @@ struct ebic_xgroup {
     size_t max_series = 0;
     unsigned char* d_base = nullptr;  // accumulator allocation (own or IPC-opened)
     unsigned char* shm = nullptr;     // mapped result block
+    unsigned char* dev_shm = nullptr; // its device address
     size_t shm_bytes = 0;
     std::string shm_name;
     unsigned long long last_seq = 0;
@@ -1578,6 +1579,7 @@ int ebic_xgroup_join(ebic_ctx* ctx, const void* handle, const char* shm_name, in
             else cudaFree(grp->d_base);
             cuda_check(e, "cudaHostRegister of the shared result block");
         }
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&grp->dev_shm), grp->shm, 0));
         grp->last_seq = *reinterpret_cast<volatile unsigned long long*>(grp->shm);
         *group_out = grp.release();
     });
@@ -1593,8 +1595,7 @@ void xgroup_launch(ebic_xgroup* g, const uint64_t* d_off, const uint16_t* d_cols
     if (P > g->max_series) fail(EBIC_ERR_INVALID_ARGUMENT, "population larger than the group's max_series");
     if (P > kMaxSeriesPerLaunch || L > kMaxLenPerLaunch)
         fail(EBIC_ERR_INVALID_ARGUMENT, "batch exceeds 2048 series / 8192 columns; split it");
-    unsigned char* dev_shm = nullptr;
-    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev_shm), g->shm, 0));
+    unsigned char* dev_shm = g->dev_shm;
     auto* counts = reinterpret_cast<uint64_t*>(dev_shm + 128);
     auto* fit = want_fit ? reinterpret_cast<double*>(dev_shm + 128 + 8 * g->max_series) : nullptr;
     auto* ticket = reinterpret_cast<unsigned int*>(g->d_base);
