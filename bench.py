@@ -374,13 +374,28 @@ def run_ours(args):
         import uuid
         handle = (C.c_ubyte * 64)()
         name = f"/ebic_bench_{os.getpid()}_{uuid.uuid4().hex[:8]}"
+        ok = 1
         if rank == 0:
-            _lib.check(_lib.lib.ebic_xgroup_create(ev.handle, 2048, name.encode(), handle))
-        obj = [bytes(handle), name]
+            ok = int(_lib.lib.ebic_xgroup_create(ev.handle, 2048, name.encode(), handle) == 0)
+        obj = [bytes(handle), name, ok]
         dist.broadcast_object_list(obj, src=0)
         xgroup = _lib.vp()
-        _lib.check(_lib.lib.ebic_xgroup_join(ev.handle, (C.c_ubyte * 64).from_buffer_copy(obj[0]),
-                                             obj[1].encode(), world, 2048, C.byref(xgroup)))
+        if obj[2]:
+            ok = int(_lib.lib.ebic_xgroup_join(ev.handle, (C.c_ubyte * 64).from_buffer_copy(obj[0]),
+                                               obj[1].encode(), world, 2048, C.byref(xgroup)) == 0)
+        else:
+            ok = 0
+        # every rank must agree (IPC may be unavailable in a container)
+        agree = torch.tensor([ok], dtype=torch.int32, device=dev if args.backend == "nccl" else "cpu")
+        dist.all_reduce(agree, op=dist.ReduceOp.MIN)
+        if not int(agree.item()):
+            if ok:
+                _lib.check(_lib.lib.ebic_xgroup_destroy(xgroup))
+            print(f"[bench] rank {rank}: in-kernel cross-rank sum unavailable "
+                  f"({_lib.lib.ebic_last_error().decode()}); e2e not measured", file=sys.stderr)
+            xgroup = None
+            if args.reduce == "kernel":
+                args.reduce = "collective"
         dist.barrier()
     xg = xgroup if args.reduce == "kernel" else None
     xseq = [0]
@@ -536,7 +551,7 @@ def run_ours(args):
     # (ebic_xgroup_evaluate: host CBF staged in-kernel, every rank's count,
     # the last rank's kernel writes counts + fitness to shared host memory) ----
     e2e_sh = None
-    if sharded:
+    if sharded and xgroup is not None:
         n_sh = 0
         el = 0.0
         host_pops = [(np.ascontiguousarray(off, dtype=np.uint64), np.ascontiguousarray(cols, dtype=np.uint16))

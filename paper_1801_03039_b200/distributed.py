@@ -86,18 +86,31 @@ class RowShardedEvaluator:
         self._local = local_counter
 
     def _join_group(self) -> None:
-        """Rank 0 creates the accumulator + shared block; everyone joins."""
+        """Rank 0 creates the accumulator + shared block; everyone joins.  If
+        any rank cannot (no CUDA IPC in the container, no /dev/shm), all ranks
+        fall back to the collective."""
+        import torch
         handle = (C.c_ubyte * 64)()
         name = f"/ebic_{os.getpid()}_{uuid.uuid4().hex[:12]}"
+        ok = 1
         if self.rank == 0:
-            check(lib.ebic_xgroup_create(self._ev.handle, self.max_series, name.encode(), handle))
-        obj = [bytes(handle), name]
+            ok = int(lib.ebic_xgroup_create(self._ev.handle, self.max_series, name.encode(), handle) == 0)
+        obj = [bytes(handle), name, ok]
         self.dist.broadcast_object_list(obj, src=self._src(), group=self.group)
-        hb = (C.c_ubyte * 64).from_buffer_copy(obj[0])
         g = vp()
-        check(lib.ebic_xgroup_join(self._ev.handle, hb, obj[1].encode(), self.world, self.max_series,
-                                   C.byref(g)))
-        self._xg = g
+        ok = 0
+        if obj[2]:
+            hb = (C.c_ubyte * 64).from_buffer_copy(obj[0])
+            ok = int(lib.ebic_xgroup_join(self._ev.handle, hb, obj[1].encode(), self.world,
+                                          self.max_series, C.byref(g)) == 0)
+        backend = self.dist.get_backend(self.group)
+        agree = torch.tensor([ok], dtype=torch.int32,
+                             device="cuda" if backend == "nccl" else "cpu")
+        self.dist.all_reduce(agree, op=self.dist.ReduceOp.MIN, group=self.group)
+        if int(agree.item()):
+            self._xg = g
+        elif ok:
+            check(lib.ebic_xgroup_destroy(g))
         self.dist.barrier(group=self.group)
 
     def _src(self) -> int:
