@@ -39,47 +39,46 @@
 
 namespace ebic {
 
+// fitness.hpp:20-39 -- the reference's row partition for its thread pool.
+// The B200 path shards rows across devices instead; counts are partition
+// invariant (fitness.hpp:17-19), so a plan is accepted for signature parity
+// and never changes a result.  Same chunks as the reference: ceil(n / w)
+// rows each, the last one short.
 struct RowRange {
     std::size_t lo = 0;
     std::size_t hi = 0;
 };
 
-// Row partition of the reference (fitness.hpp:30-39).  The B200 path shards
-// rows across devices instead; counts are partition invariant, so the plan is
-// accepted for signature parity and never changes a result.
 struct ChunkPlan {
     std::vector<RowRange> chunks;
     unsigned worker_count = 1;
 };
 
-inline ChunkPlan make_chunk_plan(std::size_t n_rows, unsigned workers = 0) {
-    if (n_rows == 0) throw std::invalid_argument("matrix has no rows");
-    if (workers == 0) workers = std::max(1u, std::thread::hardware_concurrency());
-    ChunkPlan plan;
-    plan.worker_count = workers;
-    const std::size_t chunk = (n_rows + workers - 1) / workers;
-    for (std::size_t lo = 0; lo < n_rows; lo += chunk)
-        plan.chunks.push_back({lo, std::min(lo + chunk, n_rows)});
-    return plan;
+inline ChunkPlan make_chunk_plan(std::size_t rows, unsigned workers = 0) {
+    if (!rows) throw std::invalid_argument("matrix has no rows");
+    const unsigned w = workers ? workers : std::max(1u, std::thread::hardware_concurrency());
+    const std::size_t step = rows / w + (rows % w != 0);
+    ChunkPlan out;
+    out.worker_count = w;
+    out.chunks.reserve((rows + step - 1) / step);
+    for (std::size_t at = 0; at < rows; at += step) out.chunks.push_back(RowRange{at, std::min(rows, at + step)});
+    return out;
 }
 
+// fitness.hpp:41-52 -- sigma: the expected-support scale of Eq. 1.
 struct FitnessParams {
     std::uint64_t sigma = 4;
 };
 
-inline std::uint64_t default_sigma(std::size_t n_rows) { return ebic_default_sigma(n_rows); }
+inline std::uint64_t default_sigma(std::size_t rows) { return ebic_default_sigma(rows); }
 
-// Single-row predicate (fitness.hpp:57-67); host side, used by tests and by
-// code that checks one row.  Same fp64 add-then-compare form.
-inline bool row_matches(const ExpressionMatrix& m, std::size_t row,
-                        std::span<const ColumnIndex> series, double epsilon = 0.0) {
-    const double* v = m.row_ptr(row);
-    double prev = v[series[0]];
-    for (std::size_t i = 1; i < series.size(); ++i) {
-        const double cur = v[series[i]];
-        if (!(prev < cur + epsilon)) return false;
-        prev = cur;
-    }
+// fitness.hpp:57-67 -- one row, on the host (tests and single-row checks);
+// the same fp64 add-then-compare over adjacent pairs, first failure ends it.
+inline bool row_matches(const ExpressionMatrix& matrix, std::size_t row,
+                        std::span<const ColumnIndex> cols, double eps = 0.0) {
+    const double* r = matrix.row_ptr(row);
+    for (std::size_t k = 1; k < cols.size(); ++k)
+        if (!(r[cols[k - 1]] < r[cols[k]] + eps)) return false;
     return true;
 }
 
