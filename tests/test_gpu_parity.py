@@ -320,3 +320,21 @@ def test_collapsed_rank_layout_with_dirty_rows(n_dirty):
             assert bits_equal(f, wf)
         info = ev.info()
     assert info.layout == (3 if n_dirty <= 64 else 2)
+
+
+@pytest.mark.parametrize("cfg", [dict(), dict(EBIC_NO_COLLAPSE="1"), dict(EBIC_LAYOUT_F64="1"),
+                                 dict(EBIC_FORCE_DIRECT="1")], ids=str)
+def test_repeated_columns_inside_a_series(cfg):
+    """count_chunk (fitness.hpp:71-93) takes any column list: a repeated column
+    compares a value with itself (v < v + eps), exactly as the reference."""
+    rng = np.random.default_rng(31)
+    rows, n_cols = 2000, 40
+    v = np.round(rng.standard_normal((rows, n_cols)), 2)
+    series = [list(map(int, rng.choice(n_cols, size=int(rng.integers(2, 9)), replace=True)))
+              for _ in range(800)]
+    pop = cbf(series)
+    with env(**cfg), eb.Evaluator(v) as ev:
+        for e in (0.0, 1e-9, 0.01, -0.01):
+            got = ev.count_matches(pop, e)
+            want = port.count_matches(v, pop.offsets, pop.col_indices, e)
+            assert (got == want).all(), e
