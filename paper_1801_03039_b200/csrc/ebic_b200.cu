@@ -906,6 +906,20 @@ void host_evaluate_xshard(ebic_ctx& ctx, const size_t* off, const uint16_t* cols
     uint64_t* m_counts = reinterpret_cast<uint64_t*>(s0.h_map + 128);
     double* m_fit = want_fit ? reinterpret_cast<double*>(s0.h_map + 128 + P * 8) : nullptr;
     const unsigned long long seq = ++s0.seq;
+    // A failure after some shards launched would leave partial sums in the
+    // accumulator and the ticket short: drain and re-zero both, then rethrow.
+    auto reset_partial = [&] {
+        for (Shard& s : ctx.shards) {
+            cudaSetDevice(s.device);
+            cudaStreamSynchronize(s.stream);
+        }
+        cudaSetDevice(s0.device);
+        cudaMemset(ctx.d_xacc, 0, ctx.xacc_cap * sizeof(unsigned long long));
+        cudaMemset(ctx.d_xticket, 0, sizeof(unsigned int));
+        cudaDeviceSynchronize();
+        (void)cudaGetLastError();
+    };
+    try {
     for (Shard& s : ctx.shards) {
         DeviceGuard g(s.device);
         grow_mapped(&s.h_in_map, &s.h_in_map_cap, in_bytes + 64);
@@ -939,6 +953,10 @@ void host_evaluate_xshard(ebic_ctx& ctx, const size_t* off, const uint16_t* cols
                 fail(EBIC_ERR_CUDA, "cross-shard count finished without its completion flag");
             }
         }
+    }
+    } catch (...) {
+        reset_partial();
+        throw;
     }
     s0.host_us[3] += us_since(tp);
     if (counts_out) std::memcpy(counts_out, m_counts, P * 8);
