@@ -514,8 +514,8 @@ void launch_tma_t(const CUtensorMap& tm, const CountParams& p, int grid, size_t 
     // The attribute is per function and device; set it only when it grows so
     // the per-generation launch path makes no extra driver calls.
     static int smem_set[64] = {0};
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
+    int dev = sh ? sh->device : 0;  // the caller's DeviceGuard made it current
+    if (!sh) CK(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64 || (int)smem > smem_set[dev]) {
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         if (dev >= 0 && dev < 64) smem_set[dev] = (int)smem;
