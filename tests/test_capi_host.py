@@ -169,3 +169,17 @@ def test_null_fitness_plateau_matches_reference_formula():
     # junk series of length 2 on a 500-row matrix.
     p = eb.null_fitness_plateau(500, 10)
     assert p >= eb.fitness_score(250, 2, eb.FitnessParams(10))
+
+
+def test_cross_rank_group_rejects_bad_arguments():
+    """ebic_xgroup_* argument checks run before any device work."""
+    import ctypes as C
+    h = (C.c_ubyte * 64)()
+    g = _lib.vp()
+    L = _lib.lib
+    assert L.ebic_xgroup_create(None, 16, b"/x", h) == _lib.EBIC_ERR_INVALID_ARGUMENT
+    assert L.ebic_xgroup_join(None, h, b"/x", 2, 16, C.byref(g)) == _lib.EBIC_ERR_INVALID_ARGUMENT
+    assert L.ebic_xgroup_count(None, None, None, 1, 1, 0.0, 4, 0, 1, None) == _lib.EBIC_ERR_INVALID_ARGUMENT
+    assert L.ebic_xgroup_wait(None, 1, 1, None, None) == _lib.EBIC_ERR_INVALID_ARGUMENT
+    assert L.ebic_xgroup_evaluate(None, None, None, 1, 4, 0.0, 1, None, None) == _lib.EBIC_ERR_INVALID_ARGUMENT
+    assert L.ebic_xgroup_destroy(None) == 0
