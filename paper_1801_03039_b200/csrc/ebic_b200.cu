@@ -896,6 +896,28 @@ inline double us_since(HostClock::time_point& t) {
     return d;
 }
 
+// The host CBF staged in a shard's mapped pinned buffer (read by the device:
+// CTA 0 copies it into d_in inside the count kernel): offsets at byte 0,
+// columns from the next 16-byte boundary.  Returns where the columns start and
+// the staged size.
+struct StagedCbf {
+    size_t cols_at = 0;
+    size_t bytes = 0;
+};
+
+StagedCbf stage_cbf(Shard& s, const size_t* off, const uint16_t* cols, size_t P) {
+    static_assert(sizeof(size_t) == sizeof(uint64_t), "size_t must be 64-bit");
+    const size_t L = off[P];
+    StagedCbf st;
+    st.cols_at = ((P + 1) * sizeof(uint64_t) + 15) & ~size_t(15);
+    st.bytes = st.cols_at + L * sizeof(uint16_t);
+    grow_mapped(&s.h_in_map, &s.h_in_map_cap, st.bytes + 64);
+    grow_device(&s.d_in, &s.d_in_cap, st.bytes + 64);
+    std::memcpy(s.h_in_map, off, (P + 1) * sizeof(uint64_t));
+    if (L) std::memcpy(s.h_in_map + st.cols_at, cols, L * sizeof(uint16_t));
+    return st;
+}
+
 // Cross-shard reduction setup: peer access from every shard's device to
 // shards[0]'s, and the accumulator (zeroed; the last arriver of each launch
 // re-zeroes what it consumes).  Returns false when unavailable.
@@ -945,9 +967,6 @@ void host_evaluate_xshard(ebic_ctx& ctx, const size_t* off, const uint16_t* cols
                           double eps, bool want_fit, uint64_t sigma, uint64_t* counts_out,
                           double* fit_out, HostClock::time_point& tp) {
     Shard& s0 = ctx.shards[0];
-    const size_t off_bytes = (P + 1) * sizeof(uint64_t);
-    const size_t cols_at = (off_bytes + 15) & ~size_t(15);
-    const size_t in_bytes = cols_at + L * sizeof(uint16_t);
     {
         DeviceGuard g(s0.device);
         grow_mapped(&s0.h_map, &s0.h_map_cap, 128 + P * 16);
@@ -971,18 +990,15 @@ void host_evaluate_xshard(ebic_ctx& ctx, const size_t* off, const uint16_t* cols
     try {
     for (Shard& s : ctx.shards) {
         DeviceGuard g(s.device);
-        grow_mapped(&s.h_in_map, &s.h_in_map_cap, in_bytes + 64);
-        grow_device(&s.d_in, &s.d_in_cap, in_bytes + 64);
-        std::memcpy(s.h_in_map, off, off_bytes);
-        if (L) std::memcpy(s.h_in_map + cols_at, cols, L * sizeof(uint16_t));
+        const StagedCbf in = stage_cbf(s, off, cols, P);
         if (s.knobs.host_copy)
-            CK(cudaMemcpyAsync(s.d_in, s.h_in_map, in_bytes, cudaMemcpyHostToDevice, s.stream));
+            CK(cudaMemcpyAsync(s.d_in, s.h_in_map, in.bytes, cudaMemcpyHostToDevice, s.stream));
         if (&s == &s0) s0.host_us[1] += us_since(tp);
         const auto* d_off = reinterpret_cast<const uint64_t*>(s.d_in);
-        const auto* d_cols = reinterpret_cast<const uint16_t*>(s.d_in + cols_at);
+        const auto* d_cols = reinterpret_cast<const uint16_t*>(s.d_in + in.cols_at);
         launch_count(ctx, s, d_off, d_cols, P, L, eps, m_counts, m_fit, sigma, s.stream, 0,
                      reinterpret_cast<unsigned long long*>(s0.h_map), seq,
-                     s.knobs.host_copy ? nullptr : s.h_in_map, in_bytes, ctx.d_xacc, ctx.d_xticket,
+                     s.knobs.host_copy ? nullptr : s.h_in_map, in.bytes, ctx.d_xacc, ctx.d_xticket,
                      static_cast<uint32_t>(ctx.shards.size()));
         if (&s == &s0) s0.host_us[2] += us_since(tp);
     }
@@ -1022,9 +1038,6 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
     validate_cbf(off, cols, P, ctx.n_cols);
     s0.host_us[0] += us_since(tp);
     const size_t L = off[P];
-    const size_t off_bytes = (P + 1) * sizeof(uint64_t);
-    const size_t cols_at = (off_bytes + 15) & ~size_t(15);
-    const size_t in_bytes = cols_at + L * sizeof(uint16_t);
     const bool single = ctx.shards.size() == 1;
     if (!single && P <= kMaxSeriesPerLaunch && L <= kMaxLenPerLaunch && setup_xshard(ctx, P)) {
         host_evaluate_xshard(ctx, off, cols, P, L, eps, want_fit, sigma, counts_out, fit_out, tp);
@@ -1032,15 +1045,12 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
     }
     for (Shard& s : ctx.shards) {
         DeviceGuard g(s.device);
-        grow_mapped(&s.h_in_map, &s.h_in_map_cap, in_bytes + 64);
         grow_mapped(&s.h_map, &s.h_map_cap, 128 + P * 16);
-        grow_device(&s.d_in, &s.d_in_cap, in_bytes + 64);
-        static_assert(sizeof(size_t) == sizeof(uint64_t), "size_t must be 64-bit");
-        // Stage the CBF in mapped pinned memory.  A single TMA launch copies it
-        // to the device itself (CTA 0, stage_host_cbf): no cudaMemcpyAsync on
-        // the per-generation path.  Otherwise one async copy.
-        std::memcpy(s.h_in_map, off, off_bytes);
-        if (L) std::memcpy(s.h_in_map + cols_at, cols, L * sizeof(uint16_t));
+        // A single TMA launch copies the staged CBF to the device itself (CTA
+        // 0, stage_host_cbf): no cudaMemcpyAsync on the per-generation path.
+        // Otherwise one async copy.
+        const StagedCbf in = stage_cbf(s, off, cols, P);
+        const size_t cols_at = in.cols_at, in_bytes = in.bytes;
         const bool one_launch = P <= kMaxSeriesPerLaunch && L <= kMaxLenPerLaunch &&
                                 !s.knobs.host_copy;
         if (!one_launch)
@@ -1733,16 +1743,10 @@ int ebic_xgroup_evaluate(ebic_xgroup* g, const size_t* offsets, const uint16_t* 
         validate_cbf(offsets, cols, n_series, ctx.n_cols);
         const size_t L = offsets[n_series];
         DeviceGuard dg(s.device);
-        const size_t off_bytes = (n_series + 1) * sizeof(uint64_t);
-        const size_t cols_at = (off_bytes + 15) & ~size_t(15);
-        const size_t in_bytes = cols_at + L * sizeof(uint16_t);
-        grow_mapped(&s.h_in_map, &s.h_in_map_cap, in_bytes + 64);
-        grow_device(&s.d_in, &s.d_in_cap, in_bytes + 64);
-        std::memcpy(s.h_in_map, offsets, off_bytes);
-        if (L) std::memcpy(s.h_in_map + cols_at, cols, L * sizeof(uint16_t));
+        const StagedCbf in = stage_cbf(s, offsets, cols, n_series);
         xgroup_launch(g, reinterpret_cast<const uint64_t*>(s.d_in),
-                      reinterpret_cast<const uint16_t*>(s.d_in + cols_at), n_series, L, eps, sigma,
-                      fitness_out != nullptr, seq, s.stream, s.h_in_map, in_bytes);
+                      reinterpret_cast<const uint16_t*>(s.d_in + in.cols_at), n_series, L, eps, sigma,
+                      fitness_out != nullptr, seq, s.stream, s.h_in_map, in.bytes);
         xgroup_wait(g, seq, n_series, counts_out, fitness_out, s.stream);
     });
 }
