@@ -338,3 +338,30 @@ def test_repeated_columns_inside_a_series(cfg):
             got = ev.count_matches(pop, e)
             want = port.count_matches(v, pop.offsets, pop.col_indices, e)
             assert (got == want).all(), e
+
+
+@pytest.mark.parametrize("cfg", [dict(), dict(EBIC_NO_COLLAPSE="1"), dict(EBIC_LAYOUT_F64="1")], ids=str)
+def test_long_series_and_overflow_length_bucket(cfg):
+    """Lengths 13-62 (generic walk) and >= 63 (the work list's overflow bucket,
+    listed in a separate pass) next to short ones, across several launches."""
+    rng = np.random.default_rng(77)
+    rows, n_cols = 3000, 300
+    v = np.round(rng.standard_normal((rows, n_cols)), 1)
+    # mostly increasing rows for some column orders so long series still match
+    v[:500] = np.sort(v[:500], axis=1)
+    lens = list(rng.integers(2, 12, size=300)) + list(rng.integers(13, 63, size=120)) + \
+        list(rng.integers(63, 250, size=40)) + [63, 64, 127, 250]
+    rng.shuffle(lens)
+    series = []
+    for L in lens:
+        if rng.random() < 0.3:  # ascending columns: matches the sorted rows
+            series.append(sorted(map(int, rng.choice(n_cols, size=int(L), replace=False))))
+        else:
+            series.append(list(map(int, rng.choice(n_cols, size=int(L), replace=False))))
+    pop = cbf(series)
+    with env(**cfg), eb.Evaluator(v) as ev:
+        for e in (0.0, 1e-9, 0.05):
+            got = ev.count_matches(pop, e)
+            want = port.count_matches(v, pop.offsets, pop.col_indices, e)
+            assert (got == want).all(), e
+            assert got.max() > 0
