@@ -365,3 +365,18 @@ def test_long_series_and_overflow_length_bucket(cfg):
             want = port.count_matches(v, pop.offsets, pop.col_indices, e)
             assert (got == want).all(), e
             assert got.max() > 0
+
+
+def test_many_rows():
+    """4.2M rows (65,600 row tiles): tile indexing, shard padding and counts
+    far above one tile, against the oracle on a small population."""
+    rng = np.random.default_rng(5)
+    rows, n_cols = 4_200_007, 24
+    v = rng.standard_normal((rows, n_cols)).astype(np.float64)
+    series = random_population(rng, n_cols, 40, max_len=6)
+    pop = cbf(series)
+    with eb.Evaluator(v) as ev:
+        for e in (0.0, 0.3):
+            got = ev.count_matches(pop, e)
+            want = port.count_matches(v, pop.offsets, pop.col_indices, e)
+            assert (got == want).all(), e
