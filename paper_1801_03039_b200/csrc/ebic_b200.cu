@@ -1653,15 +1653,24 @@ int ebic_xgroup_join(ebic_ctx* ctx, const void* handle, const char* shm_name, in
             grp->d_base = static_cast<unsigned char*>(p);
         }
         grp->shm_bytes = xgroup_shm_bytes(max_series);
-        grp->shm = map_shm(shm_name, grp->shm_bytes, false);
-        const cudaError_t e = cudaHostRegister(grp->shm, grp->shm_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
-        if (e != cudaSuccess) {
-            munmap(grp->shm, grp->shm_bytes);
-            if (!grp->owner) cudaIpcCloseMemHandle(grp->d_base);
-            else cudaFree(grp->d_base);
-            cuda_check(e, "cudaHostRegister of the shared result block");
+        // Undo what this join acquired if a later step fails.
+        auto release = [&] {
+            if (grp->shm) {
+                cudaHostUnregister(grp->shm);
+                munmap(grp->shm, grp->shm_bytes);
+            }
+            if (grp->owner) cudaFree(grp->d_base);
+            else cudaIpcCloseMemHandle(grp->d_base);
+            (void)cudaGetLastError();
+        };
+        try {
+            grp->shm = map_shm(shm_name, grp->shm_bytes, false);
+            CK(cudaHostRegister(grp->shm, grp->shm_bytes, cudaHostRegisterMapped | cudaHostRegisterPortable));
+            CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&grp->dev_shm), grp->shm, 0));
+        } catch (...) {
+            release();
+            throw;
         }
-        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&grp->dev_shm), grp->shm, 0));
         grp->last_seq = *reinterpret_cast<volatile unsigned long long*>(grp->shm);
         *group_out = grp.release();
     });
