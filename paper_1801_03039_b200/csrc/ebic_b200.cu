@@ -446,11 +446,10 @@ CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int
                 c.slice = slice;
                 c.rpg = slice / (2 * rank_planes);
                 c.rpl = rank_planes == 2 ? 4 : 8;
-                // one plane: 24 warps (no spills under the 80-register cap)
-                // measured fastest (C5 103 us vs 107 at 16, 114 at 31 with
-                // spills); two planes: 31 warps.
-                c.ncw = want_ncw ? (want_ncw == 16 ? 16 : want_ncw == 24 && rank_planes == 1 ? 24 : 32)
-                                 : (rank_planes == 1 ? 24 : 32);
+                // 24 warps (no spills under the 80-register cap) measured
+                // fastest: one plane C5 103 us vs 107 at 16, 114 at 31 with
+                // spills; two planes C5 154 us vs 169 at 16, 165 at 31.
+                c.ncw = want_ncw == 16 ? 16 : want_ncw == 32 ? 32 : 24;
                 c.spg = kn.spg == 4 ? 4 : 2;
                 if (c.spg == 4) c.ncw = 16;  // 4 walks per group need the 16-warp register budget
                 if (fit_ring(c, n_cols, slice, P, L, budget, min_stages, want_stages)) return c;
@@ -546,16 +545,18 @@ void launch_tma(const CountConfig& c, bool e0, const CUtensorMap& tm, const Coun
             CK(cudaGetLastError());
             return;
         }
+        const bool n24 = c.ncw == 24;
         if (c.layout == 2) {
             if (s64) {
                 if (n16) launch_tma_t<RankWalker<2, 64>, 16>(tm, p, grid, smem, st, sh);
+                else if (n24) launch_tma_t<RankWalker<2, 64>, 24>(tm, p, grid, smem, st, sh);
                 else launch_tma_t<RankWalker<2, 64>, 31>(tm, p, grid, smem, st, sh);
             } else {
                 if (n16) launch_tma_t<RankWalker<2, 128>, 16>(tm, p, grid, smem, st, sh);
+                else if (n24) launch_tma_t<RankWalker<2, 128>, 24>(tm, p, grid, smem, st, sh);
                 else launch_tma_t<RankWalker<2, 128>, 31>(tm, p, grid, smem, st, sh);
             }
         } else {
-            const bool n24 = c.ncw == 24;
             if (s64) {
                 if (n16) launch_tma_t<RankWalker<1, 64>, 16>(tm, p, grid, smem, st, sh);
                 else if (n24) launch_tma_t<RankWalker<1, 64>, 24>(tm, p, grid, smem, st, sh);

@@ -20,9 +20,10 @@ pytestmark = pytest.mark.gpu
 port = oracle.Port()
 
 # Every count-kernel configuration the library can select: the exact rank
-# tile (default; 1 or 2 planes by eps / NaN presence, 16 or 31 consumer warps),
+# tile (default; 1 or 2 planes by eps / NaN presence, 16, 24 or 31 consumer warps),
 # the fp64 tile (rows-per-tile x rows-per-lane), and the unstaged direct kernel.
-KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NCW="24"), dict(EBIC_NCW="32"), dict(EBIC_NO_COLLAPSE="1"), dict(EBIC_SPG="4"),
+KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NCW="24"), dict(EBIC_NCW="32"), dict(EBIC_NO_COLLAPSE="1"),
+                   dict(EBIC_NO_COLLAPSE="1", EBIC_NCW="16"), dict(EBIC_NO_COLLAPSE="1", EBIC_NCW="32"), dict(EBIC_SPG="4"),
                    dict(EBIC_SPG="4", EBIC_NO_COLLAPSE="1")] +
                   [dict(EBIC_LAYOUT_F64="1", EBIC_RPG=str(g), EBIC_RPL=str(l))
                    for g in (32, 16, 8, 4) for l in (1, 2)] +
