@@ -463,7 +463,8 @@ CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int
             c.rpg = rpg;
             c.rpl = want_rpl ? want_rpl : 2;
             if (c.rpl > 1 && rpg < 4) c.rpl = 1;
-            c.ncw = (rpg == 16 && (want_ncw == 24 || want_ncw == 32)) ? want_ncw : (rpg == 16 ? 32 : 16);
+            // 16-row tiles: 24 warps (no spills; C4 47.0 us vs 47.2 at 31, 55 at 16).
+            c.ncw = rpg == 16 ? (want_ncw == 32 ? 32 : 24) : 16;
             if (want_ncw == 16) c.ncw = 16;
             if (fit_ring(c, n_cols, size_t(rpg) * 8, P, L, budget, min_stages, want_stages)) return c;
         }

@@ -27,7 +27,7 @@ KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NCW="24"), dict(EBIC_N
                    dict(EBIC_SPG="4", EBIC_NO_COLLAPSE="1")] +
                   [dict(EBIC_LAYOUT_F64="1", EBIC_RPG=str(g), EBIC_RPL=str(l))
                    for g in (32, 16, 8, 4) for l in (1, 2)] +
-                  [dict(EBIC_LAYOUT_F64="1", EBIC_NCW="16"), dict(EBIC_FORCE_DIRECT="1")])
+                  [dict(EBIC_LAYOUT_F64="1", EBIC_NCW="16"), dict(EBIC_LAYOUT_F64="1", EBIC_NCW="32"), dict(EBIC_FORCE_DIRECT="1")])
 
 
 @contextmanager
