@@ -202,24 +202,38 @@ extern "C" int ebic_top_rank_update(size_t n_cols, size_t n_entries, const size_
                 touched[nt] = int32_t(s);
                 nt += w.alive[s] && w.len[s] > 0 && n > 0;
             }
-        } else {
-            for (const uint16_t c : w.distinct)
-                for (const int32_t s : w.post[c]) {
-                    touched[nt] = s;  // first sighting of s this candidate
-                    nt += (cnt[s]++ == 0);
-                }
         }
         const uint32_t* need = w.need.data();
         auto overlaps = [&](int32_t s) {
             return all_overlap || cnt[s] >= need[std::min<size_t>(w.len[s], n)];
         };
-        // Blocked by any present entry of equal or higher fitness that overlaps (:185-192).
+        // Blocked by any present entry of equal or higher fitness that overlaps
+        // (:185-192).  Counting stops at the first such entry: a blocked
+        // candidate evicts nothing, so the remaining counts are not needed.
         bool blocked = false;
-        for (size_t t = 0; t < nt; ++t) {
-            const int32_t s = touched[t];
-            if (w.alive[s] && w.fit[s] >= f && overlaps(s)) {
-                blocked = true;
-                break;
+        if (!all_overlap) {
+            const uint32_t* len = w.len.data();
+            const uint8_t* alive = w.alive.data();
+            const double* fit = w.fit.data();
+            for (const uint16_t c : w.distinct) {
+                for (const int32_t s : w.post[c]) {
+                    touched[nt] = s;  // first sighting of s this candidate
+                    const uint32_t k = ++cnt[s];
+                    nt += (k == 1);
+                    if (k == need[std::min<size_t>(len[s], n)] && alive[s] && fit[s] >= f) {
+                        blocked = true;
+                        break;
+                    }
+                }
+                if (blocked) break;
+            }
+        } else {
+            for (size_t t = 0; t < nt; ++t) {
+                const int32_t s = touched[t];
+                if (w.alive[s] && w.fit[s] >= f && overlaps(s)) {
+                    blocked = true;
+                    break;
+                }
             }
         }
         if (!blocked)  // evict overlapping lower-fitness entries (:194-196)
