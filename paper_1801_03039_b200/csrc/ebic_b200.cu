@@ -235,8 +235,6 @@ struct Shard {
     // about 3.5 us for a plain launch of this kernel.
     struct GraphSlot {
         const void* func = nullptr;
-        int grid = 0, block = 0;
-        size_t smem = 0;
         cudaGraph_t g = nullptr;
         cudaGraphExec_t exec = nullptr;
         cudaGraphNode_t node = nullptr;
@@ -484,21 +482,28 @@ void launch_kernel(Shard* sh, const void* func, int grid, int block, size_t smem
     kp.blockDim = dim3(block);
     kp.sharedMemBytes = static_cast<unsigned>(smem);
     kp.kernelParams = args;
-    for (Shard::GraphSlot& g : sh->graphs)
-        if (g.func == func && g.grid == grid && g.block == block && g.smem == smem) {
-            CK(cudaGraphExecKernelNodeSetParams(g.exec, g.node, &kp));
+    // One graph per kernel function: the parameter update re-points it at
+    // this launch's grid, block and dynamic shared memory as well (the GA's
+    // population and series lengths change the ring's size every generation).
+    for (size_t i = 0; i < sh->graphs.size(); ++i) {
+        Shard::GraphSlot& g = sh->graphs[i];
+        if (g.func != func) continue;
+        if (cudaGraphExecKernelNodeSetParams(g.exec, g.node, &kp) == cudaSuccess) {
             CK(cudaGraphLaunch(g.exec, st));
             return;
         }
+        (void)cudaGetLastError();  // not updatable: rebuild below
+        cudaGraphExecDestroy(g.exec);
+        cudaGraphDestroy(g.g);
+        sh->graphs.erase(sh->graphs.begin() + static_cast<std::ptrdiff_t>(i));
+        break;
+    }
     Shard::GraphSlot g;
     g.func = func;
-    g.grid = grid;
-    g.block = block;
-    g.smem = smem;
     CK(cudaGraphCreate(&g.g, 0));
     CK(cudaGraphAddKernelNode(&g.node, g.g, nullptr, 0, &kp));
     CK(cudaGraphInstantiate(&g.exec, g.g, 0));
-    if (sh->graphs.size() >= 16) {  // bounded: drop the oldest shape
+    if (sh->graphs.size() >= 16) {  // bounded: drop the oldest function
         cudaGraphExecDestroy(sh->graphs.front().exec);
         cudaGraphDestroy(sh->graphs.front().g);
         sh->graphs.erase(sh->graphs.begin());
