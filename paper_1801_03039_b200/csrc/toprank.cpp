@@ -50,12 +50,12 @@ struct Workspace {
     std::vector<int64_t> ref;         // >= 0: existing entry index; < 0: -(candidate + 1)
     std::vector<uint8_t> alive;
     std::vector<std::vector<int32_t>> post;  // per column: slots containing it
-    std::vector<uint32_t> cnt;        // per slot: intersection with the current candidate
-    std::vector<int32_t> touched;
+    std::vector<uint64_t> cnt;        // per slot: (visit << 32) | intersection with that candidate
+    std::vector<int32_t> touched, all;
     std::vector<uint32_t> stamp;      // per column: last series that used it (dedupe)
     std::vector<uint32_t> need;       // per length: least overlapping intersection
     std::vector<uint16_t> distinct;
-    std::vector<std::pair<uint64_t, uint32_t>> order, order_tmp;  // (~fitness bits, index)
+    std::vector<uint64_t> order, order_tmp;  // (high half of ~fitness bits, index)
 };
 
 Workspace& workspace() {
@@ -119,7 +119,7 @@ extern "C" int ebic_top_rank_update(size_t n_cols, size_t n_entries, const size_
     if (w.stamp.size() < n_cols) w.stamp.resize(n_cols);
     std::fill(w.stamp.begin(), w.stamp.begin() + n_cols, 0u);
     if (w.cnt.size() < n_slots_max) w.cnt.resize(n_slots_max);
-    std::fill(w.cnt.begin(), w.cnt.begin() + n_slots_max, 0u);
+    std::fill(w.cnt.begin(), w.cnt.begin() + n_slots_max, uint64_t{0});
     w.touched.resize(n_slots_max + 1);
     uint32_t stamp_id = 0;
 
@@ -157,29 +157,43 @@ extern "C" int ebic_top_rank_update(size_t n_cols, size_t n_entries, const size_
     }
 
     // Visiting order: positive fitness only, fitness desc then index asc
-    // (:172-179).  The bit pattern of a positive double orders like its value,
-    // so a stable LSD radix sort of ~bits over candidates taken in index order
-    // gives exactly that order (equal fitness <=> equal bits for x > 0).
+    // (:172-179).  The bit pattern of a positive double orders like its value.
+    // Keys are (high half of ~bits, index): a stable LSD radix sort over their
+    // high 32 bits, then runs that tie there are finished by the full order
+    // (equal fitness <=> equal bits for x > 0; such runs stay in index order).
     w.order.clear();
     for (size_t i = 0; i < n_cand; ++i)
         if (cand_fitness[i] > 0.0) {
             uint64_t bits;
             std::memcpy(&bits, &cand_fitness[i], sizeof bits);
-            w.order.push_back({~bits, uint32_t(i)});
+            w.order.push_back(((~bits) & 0xffffffff00000000ull) | uint64_t(i));
         }
     w.order_tmp.resize(w.order.size());
-    for (int shift = 0; shift < 64; shift += 8) {
+    for (int shift = 32; shift < 64; shift += 8) {
         uint32_t hist[256] = {};
-        for (const auto& o : w.order) ++hist[(o.first >> shift) & 0xff];
-        if (hist[(w.order.empty() ? 0 : w.order[0].first >> shift) & 0xff] == w.order.size()) continue;
+        for (const uint64_t o : w.order) ++hist[(o >> shift) & 0xff];
+        if (hist[(w.order.empty() ? 0 : w.order[0] >> shift) & 0xff] == w.order.size()) continue;
         uint32_t at = 0;
         for (uint32_t& h : hist) {
             const uint32_t c = h;
             h = at;
             at += c;
         }
-        for (const auto& o : w.order) w.order_tmp[hist[(o.first >> shift) & 0xff]++] = o;
+        for (const uint64_t o : w.order) w.order_tmp[hist[(o >> shift) & 0xff]++] = o;
         w.order.swap(w.order_tmp);
+    }
+    auto before = [&](uint64_t x, uint64_t y) {  // full visiting order
+        const double fx = cand_fitness[uint32_t(x)], fy = cand_fitness[uint32_t(y)];
+        return fx != fy ? fx > fy : uint32_t(x) < uint32_t(y);
+    };
+    for (size_t i = 1; i < w.order.size(); ++i) {  // insertion within tied runs
+        const uint64_t x = w.order[i];
+        size_t j = i;
+        while (j > 0 && (w.order[j - 1] >> 32) == (x >> 32) && before(x, w.order[j - 1])) {
+            w.order[j] = w.order[j - 1];
+            --j;
+        }
+        w.order[j] = x;
     }
 
     // The reference does not validate the threshold here (run() does, :48-49).
@@ -187,79 +201,99 @@ extern "C" int ebic_top_rank_update(size_t n_cols, size_t n_entries, const size_
     // and the posting lists see every candidate pair that matters; a negative
     // threshold makes every pair of non-empty series overlap (0/m > thr), and
     // an empty series never does (0/0 is NaN).
+    //
+    // Intersection counts carry the candidate's visit number in their high
+    // half, so they need no reset between candidates.  Entries that reach the
+    // overlap bound with a lower fitness are noted as they are found and
+    // evicted once the candidate is known to be admitted.
     const bool all_overlap = overlap_threshold < 0.0;
+    const uint32_t* need = w.need.data();
     uint64_t next = *next_seq;
-    for (const auto& o : w.order) {
-        const uint32_t p = o.second;
+    uint64_t visit = 0;
+    for (const uint64_t o : w.order) {
+        const uint32_t p = uint32_t(o);
         const double f = cand_fitness[p];
         const size_t n = cand_offsets[p + 1] - cand_offsets[p];
         distinct_cols(cand_cols + cand_offsets[p], n);
-        size_t nt = 0;
-        int32_t* touched = w.touched.data();
-        uint32_t* cnt = w.cnt.data();
-        if (all_overlap) {
-            for (size_t s = 0; s < w.fit.size(); ++s) {
-                touched[nt] = int32_t(s);
-                nt += w.alive[s] && w.len[s] > 0 && n > 0;
-            }
-        }
-        const uint32_t* need = w.need.data();
-        auto overlaps = [&](int32_t s) {
-            return all_overlap || cnt[s] >= need[std::min<size_t>(w.len[s], n)];
-        };
-        // Blocked by any present entry of equal or higher fitness that overlaps
-        // (:185-192).  Counting stops at the first such entry: a blocked
-        // candidate evicts nothing, so the remaining counts are not needed.
+        int32_t* lower = w.touched.data();  // overlapping entries of lower fitness
+        size_t n_lower = 0;
         bool blocked = false;
-        if (!all_overlap) {
+        if (all_overlap) {
+            const bool any = n > 0;
+            for (size_t s = 0; s < w.fit.size() && any; ++s) {
+                if (!w.alive[s] || w.len[s] == 0) continue;
+                if (w.fit[s] >= f) {
+                    blocked = true;
+                    break;
+                }
+                lower[n_lower++] = int32_t(s);
+            }
+        } else {
+            const uint64_t tag = ++visit << 32;
+            uint64_t* cnt = w.cnt.data();
             const uint32_t* len = w.len.data();
             const uint8_t* alive = w.alive.data();
             const double* fit = w.fit.data();
             for (const uint16_t c : w.distinct) {
                 for (const int32_t s : w.post[c]) {
-                    touched[nt] = s;  // first sighting of s this candidate
-                    const uint32_t k = ++cnt[s];
-                    nt += (k == 1);
-                    if (k == need[std::min<size_t>(len[s], n)] && alive[s] && fit[s] >= f) {
+                    const uint64_t v = cnt[s];
+                    const uint64_t k = (v & 0xffffffff00000000ull) == tag ? v + 1 : tag + 1;
+                    cnt[s] = k;
+                    if (uint32_t(k) != need[std::min<size_t>(len[s], n)] || !alive[s]) continue;
+                    if (fit[s] >= f) {
                         blocked = true;
                         break;
                     }
+                    lower[n_lower++] = s;
                 }
                 if (blocked) break;
             }
-        } else {
-            for (size_t t = 0; t < nt; ++t) {
-                const int32_t s = touched[t];
-                if (w.alive[s] && w.fit[s] >= f && overlaps(s)) {
-                    blocked = true;
-                    break;
-                }
-            }
         }
-        if (!blocked)  // evict overlapping lower-fitness entries (:194-196)
-            for (size_t t = 0; t < nt; ++t) {
-                const int32_t s = touched[t];
-                if (w.fit[s] < f && overlaps(s)) w.alive[s] = 0;
-            }
-        if (!all_overlap)
-            for (size_t t = 0; t < nt; ++t) cnt[touched[t]] = 0;
-        if (!blocked) add_slot(f, next++, uint32_t(n), -int64_t(p) - 1);  // (:197-198)
+        if (!blocked) {  // evict overlapping lower-fitness entries (:194-196), admit (:197-198)
+            for (size_t t = 0; t < n_lower; ++t) w.alive[lower[t]] = 0;
+            add_slot(f, next++, uint32_t(n), -int64_t(p) - 1);
+        }
     }
     *next_seq = next;
 
-    // Final order (fitness desc, seq asc) and truncation (:201-205).
-    size_t n_alive = 0;
-    for (size_t s = 0; s < w.fit.size(); ++s)
-        if (w.alive[s]) w.touched[n_alive++] = int32_t(s);
+    // Final order (fitness desc, seq asc) and truncation (:201-205).  Slots
+    // admitted here already come in that order with sequence numbers above
+    // every entry's; when the entries do too (the list's own invariant) the
+    // result is a merge, else a partial sort.
+    auto first = [&](int32_t a, int32_t b) {
+        if (w.fit[a] != w.fit[b]) return w.fit[a] > w.fit[b];
+        return w.seq[a] < w.seq[b];
+    };
+    int32_t* old_alive = w.touched.data();
+    int32_t* new_alive = old_alive + n_entries;
+    size_t n_old = 0, n_new = 0;
+    bool sorted = true;
+    for (size_t s = 0; s < n_entries; ++s)
+        if (w.alive[s]) {
+            if (n_old && !first(old_alive[n_old - 1], int32_t(s))) sorted = false;
+            old_alive[n_old++] = int32_t(s);
+        }
+    for (size_t s = n_entries; s < w.fit.size(); ++s)
+        if (w.alive[s]) new_alive[n_new++] = int32_t(s);
+    const size_t n_alive = n_old + n_new;
     const size_t keep = std::min(capacity, n_alive);
-    std::partial_sort(w.touched.begin(), w.touched.begin() + keep, w.touched.begin() + n_alive,
-                      [&](int32_t a, int32_t b) {
-                          if (w.fit[a] != w.fit[b]) return w.fit[a] > w.fit[b];
-                          return w.seq[a] < w.seq[b];
-                      });
-    for (size_t i = 0; i < keep; ++i) {
-        out_ref[i] = w.ref[w.touched[i]];
-        out_seq[i] = w.seq[w.touched[i]];
+    if (sorted) {
+        size_t i = 0, j = 0;
+        for (size_t r = 0; r < keep; ++r) {
+            const bool take_new = i == n_old || (j < n_new && first(new_alive[j], old_alive[i]));
+            const int32_t s = take_new ? new_alive[j++] : old_alive[i++];
+            out_ref[r] = w.ref[s];
+            out_seq[r] = w.seq[s];
+        }
+    } else {
+        std::vector<int32_t>& all = w.all;
+        all.assign(old_alive, old_alive + n_old);
+        all.insert(all.end(), new_alive, new_alive + n_new);
+        std::partial_sort(all.begin(), all.begin() + keep, all.end(), first);
+        for (size_t r = 0; r < keep; ++r) {
+            out_ref[r] = w.ref[all[r]];
+            out_seq[r] = w.seq[all[r]];
+        }
     }
     *out_count = keep;
     return EBIC_OK;

@@ -156,3 +156,59 @@ def test_column_out_of_range_is_rejected():
     top = TopRankList(10)
     with pytest.raises(ValueError, match="column out of range"):
         top.update([[0, 12]], [1.0], 0.75, 100)
+
+
+def _raw_update(n_cols, entries, off, cols, fit, thr, cap, next_seq):
+    """ebic_top_rank_update called directly (entries in any order)."""
+    import ctypes as C
+    from paper_1801_03039_b200 import _lib as L
+    e_off, e_cols, e_fit, e_seq = (np.ascontiguousarray(entries[0], np.uint64),
+                                   np.ascontiguousarray(entries[1], np.uint16),
+                                   np.ascontiguousarray(entries[2], np.float64),
+                                   np.ascontiguousarray(entries[3], np.uint64))
+    pad = lambda a: a if a.size else np.zeros(1, dtype=a.dtype)  # noqa: E731
+    p = lambda a, t: a.ctypes.data_as(t)  # noqa: E731
+    k_off, k_cols, k_fit = (np.ascontiguousarray(off, np.uint64), pad(np.ascontiguousarray(cols, np.uint16)),
+                            np.ascontiguousarray(fit, np.float64))
+    n_e, n_c = len(e_fit), len(k_fit)
+    slots = max(1, min(cap, n_e + n_c))
+    ref, seq = np.zeros(slots, np.int64), np.zeros(slots, np.uint64)
+    nxt, n = C.c_uint64(next_seq), C.c_size_t(0)
+    L.check(L.lib.ebic_top_rank_update(n_cols, n_e, p(e_off, L.szp), p(pad(e_cols), L.u16p), p(pad(e_fit), L.f64p),
+                                       p(pad(e_seq), L.u64p), n_c, p(k_off, L.szp), p(k_cols, L.u16p),
+                                       p(pad(k_fit), L.f64p), float(thr), cap, C.byref(nxt), p(ref, L.i64p),
+                                       p(seq, L.u64p), C.byref(n)))
+    return ref[:n.value], seq[:n.value], nxt.value
+
+
+@pytest.mark.parametrize("shuffled", [False, True])
+def test_entries_in_any_order_match_oracle(shuffled):
+    """The final order is a merge when the entries keep the list's own order
+    (fitness desc, seq asc) and a sort otherwise; both agree with the oracle."""
+    port = oracle.Port()
+    for seed in range(40):
+        rng = np.random.default_rng(9100 + seed)
+        n_cols = int(rng.integers(6, 80))
+        def pop(n):
+            series = [rng.choice(n_cols, size=int(rng.integers(2, 6)), replace=False) for _ in range(n)]
+            off = np.zeros(n + 1, np.uint64)
+            off[1:] = np.cumsum([len(s) for s in series]) if n else []
+            cols = np.concatenate(series).astype(np.uint16) if n else np.zeros(0, np.uint16)
+            return off, cols, rng.integers(1, 6, size=n).astype(np.float64)
+        n_e = int(rng.integers(0, 30))
+        e_off, e_cols, e_fit = pop(n_e)
+        e_seq = rng.permutation(1000)[:n_e].astype(np.uint64)
+        if not shuffled:  # the list's own invariant
+            order = sorted(range(n_e), key=lambda i: (-e_fit[i], e_seq[i]))
+            segs = [e_cols[int(e_off[i]):int(e_off[i + 1])] for i in order]
+            e_off = np.zeros(n_e + 1, np.uint64)
+            e_off[1:] = np.cumsum([len(s) for s in segs]) if n_e else []
+            e_cols = np.concatenate(segs).astype(np.uint16) if n_e else np.zeros(0, np.uint16)
+            e_fit, e_seq = e_fit[order], e_seq[order]
+        off, cols, fit = pop(int(rng.integers(0, 40)))
+        thr, cap = float(rng.choice([0.3, 0.5, 0.75, 1.0])), int(rng.choice([3, 10, 100]))
+        ent = (e_off, e_cols, e_fit, e_seq)
+        got = _raw_update(n_cols, ent, off, cols, fit, thr, cap, 1000)
+        want = port.top_rank_update(n_cols, ent, off, cols, fit, thr, cap, 1000)
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]), seed
+        assert got[2] == want[2], seed
