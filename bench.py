@@ -216,20 +216,34 @@ def workload_config(t, args):
 
 
 # ---------------------------------------------------------------------------
-def large_roofline(args, peak):
-    """Roofline of the count kernel on BASELINE config 5 (200,000 x 1000, the
-    scaling-sweep matrix): its tile (800 MB in the rank layout) exceeds the
-    126 MB L2, so back-to-back steps are HBM-cold without eviction and the
-    per-launch host/launch overhead is amortised.  Reported beside the
-    headline C4 line (where one step is ~10 us of HBM time plus a ~5.5 us
-    event/launch floor)."""
+def large_roofline(args, peak, evict, sharded=False, world=1, rank=0, backend="nccl"):
+    """BASELINE config 5 (200,000 x 1000, the scaling-sweep matrix).
+
+    * Roofline of the count kernel (one GPU): its tile (400 MB in the rank
+      layout) exceeds the 126 MB L2, so back-to-back launches between one
+      event pair are HBM-cold and the per-launch overhead is amortised.
+      Reported beside the headline C4 line (where one step is ~10 us of HBM
+      time plus a ~5.5 us event/launch floor).
+    * `row_sharded`: the config-5 sweep itself -- rows sharded over the ranks
+      (1 at N=1), every step one count launch per rank plus, at N>1, the NCCL
+      all-reduce of the counts and the Eq. 1 kernel; per-step CUDA events with
+      L2 evicted before each step (a shard of 200,000/N rows fits L2 at N=8),
+      max over ranks.  Same measurement at every N, so the driver's N-sweep
+      of this key is the config-5 scaling curve."""
     import torch
+    import torch.distributed as dist
     import paper_1801_03039_b200 as eb
     from paper_1801_03039_b200 import _lib
     t = load_workload("c5")
     values = t.matrix()
-    ev = eb.Evaluator(values)
+    R = values.shape[0]
     dev = torch.device("cuda", torch.cuda.current_device())
+    lo, hi = eb.shard_range(R, world, rank) if sharded else (0, R)
+    if sharded:
+        ev = eb.Evaluator(values[lo:hi], devices=[dev.index], shard=(lo, R))
+    else:
+        ev = eb.Evaluator(values, devices=[dev.index])
+    del values
     stream = torch.cuda.current_stream(dev)
     bs = []
     for off, cols, counts, fit in t.batches:
@@ -240,18 +254,61 @@ def large_roofline(args, peak):
                        fit=torch.zeros(len(off) - 1, dtype=torch.float64, device=dev)))
 
     def step(b):
-        _lib.check(_lib.lib.ebic_count_matches_device(
-            ev.handle, b["off"].data_ptr(), b["cols"].data_ptr(), b["P"], b["L"], t.eps, t.sigma,
-            b["counts"].data_ptr(), b["fit"].data_ptr(), stream.cuda_stream))
+        if sharded:
+            _lib.check(_lib.lib.ebic_count_matches_device(
+                ev.handle, b["off"].data_ptr(), b["cols"].data_ptr(), b["P"], b["L"], t.eps, t.sigma,
+                b["counts"].data_ptr(), None, stream.cuda_stream))
+            dist.all_reduce(b["counts"], op=dist.ReduceOp.SUM)
+            _lib.check(_lib.lib.ebic_fitness_device(
+                ev.handle, b["counts"].data_ptr(), b["off"].data_ptr(), b["P"], t.sigma,
+                b["fit"].data_ptr(), stream.cuda_stream))
+        else:
+            _lib.check(_lib.lib.ebic_count_matches_device(
+                ev.handle, b["off"].data_ptr(), b["cols"].data_ptr(), b["P"], b["L"], t.eps, t.sigma,
+                b["counts"].data_ptr(), b["fit"].data_ptr(), stream.cuda_stream))
 
     for k in range(4):
         step(bs[k % len(bs)])
     torch.cuda.synchronize()
-    for b in bs:
+    for b, (_, _, _, want_fit) in zip(bs, t.batches):
         step(b)
         torch.cuda.synchronize()
         assert (b["counts"].cpu().numpy().astype(np.uint64) == b["want"]).all(), "C5 count mismatch"
+        assert (b["fit"].cpu().numpy().view(np.uint64) == want_fit.view(np.uint64)).all(), "C5 fitness mismatch"
     layout = ev.info().layout
+
+    # row-sharded sweep measurement (every N)
+    n_sh = max(20, min(args.steps // 10, 100))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_sh)]
+    if sharded:
+        dist.barrier()
+    torch.cuda.synchronize()
+    series_sh = 0
+    for k in range(n_sh):
+        b = bs[k % len(bs)]
+        evict()
+        torch.cuda._sleep(100_000)
+        evs[k][0].record(stream)
+        step(b)
+        evs[k][1].record(stream)
+        series_sh += b["P"]
+    torch.cuda.synchronize()
+    sh_ms = float(sum(e0.elapsed_time(e1) for e0, e1 in evs))
+    if sharded:
+        tt = torch.tensor([sh_ms], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        sh_ms = float(tt.item())
+    row_sharded = {"value": series_sh / (sh_ms / 1e3), "unit": UNIT, "n_gpus": world,
+                   "us_per_step": sh_ms * 1e3 / n_sh, "steps": n_sh, "rows_per_gpu": hi - lo,
+                   "reduce": (f"{backend} all-reduce of the counts + Eq. 1 kernel" if sharded
+                              else "none (1 GPU)"),
+                   "timing": "per-step CUDA events, L2 evicted before each step, max over ranks",
+                   "parity": "counts and fitness bit-exact vs the reference trace on every batch"}
+    if sharded:
+        ev.close()
+        return {"workload": "c5: synthetic 200000x1000 (5 planted 6000x30 trend blocks, seed 2026+1), "
+                            "reference GA batches", "row_sharded": row_sharded}
+
     nbytes = 0
     steps = max(20, min(args.steps // 20, 200))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -260,7 +317,7 @@ def large_roofline(args, peak):
     for k in range(steps):
         b = bs[k % len(bs)]
         step(b)
-        nbytes += algorithmic_bytes(values.shape[0], b["off_np"], b["cols_np"], LAYOUT_CELL_BYTES[layout])
+        nbytes += algorithmic_bytes(R, b["off_np"], b["cols_np"], LAYOUT_CELL_BYTES[layout])
     e1.record(stream)
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / steps
@@ -269,7 +326,7 @@ def large_roofline(args, peak):
     # The kernel stages whole row tiles (every column, read once): the DRAM
     # bytes it actually moves per launch, against the algorithmic bytes above
     # (only the columns some series uses).
-    staged = values.shape[0] * values.shape[1] * LAYOUT_CELL_BYTES[layout]
+    staged = R * ev.n_cols * LAYOUT_CELL_BYTES[layout]
     ev.close()
     return {"workload": "c5: synthetic 200000x1000 (5 planted 6000x30 trend blocks, seed 2026+1), "
                         "reference GA batches", "bound": "hbm", "achieved": achieved, "peak": peak,
@@ -278,7 +335,8 @@ def large_roofline(args, peak):
             "staged_bytes_per_launch": staged,
             "staged_GBps": staged / (us / 1e6) / 1e9, "staged_frac": staged / (us / 1e6) / 1e9 / peak,
             "biclusters_per_s": series / (us * steps / 1e6), "steps": steps,
-            "timing": "back-to-back launches between one CUDA event pair (inputs > L2)"}
+            "timing": "back-to-back launches between one CUDA event pair (inputs > L2)",
+            "row_sharded": row_sharded}
 
 
 def run_e2e_driver(t, args):
@@ -516,6 +574,13 @@ def run_ours(args):
     peak, peak_src = hbm_peak()
     info = ev.info()
 
+    # ---- BASELINE config 5: kernel roofline (1 GPU) and the row-sharded sweep
+    # (every N).  Measured before the cross-rank e2e below. ----
+    big = None
+    if not args.no_large:
+        big = large_roofline(args, peak, evict_l2, sharded=sharded, world=world, rank=rank,
+                             backend=args.backend)
+
     # ---- e2e (headline): the public C ABI from a C++ caller -- the view of the
     # reference's GA loop through include/ebic/fitness.hpp -- host buffers,
     # pinned H2D of the CBF, the kernel, results back in host memory, L2
@@ -550,8 +615,7 @@ def run_ours(args):
     # ---- e2e at N ranks: the host path through the in-kernel cross-rank sum
     # (ebic_xgroup_evaluate: host CBF staged in-kernel, every rank's count,
     # the last rank's kernel writes counts + fitness to shared host memory) ----
-    e2e_sh = None
-    if sharded and xgroup is not None:
+    def sharded_e2e():
         n_sh = 0
         el = 0.0
         host_pops = [(np.ascontiguousarray(off, dtype=np.uint64), np.ascontiguousarray(cols, dtype=np.uint16))
@@ -583,17 +647,27 @@ def run_ours(args):
         pb = [len(off) - 1 for off, _ in host_pops]
         lb = [int(off[-1]) for off, _ in host_pops]
         nb = len(host_pops)
-        e2e_sh = {"value": n_sh / el, "unit": UNIT,
-                  "h2d_bytes_per_step": int(sum((p + 1) * 8 + l * 2 for p, l in zip(pb, lb)) / nb),
-                  "d2h_bytes_per_step": int(sum(16 * p for p in pb) / nb),
-                  "us_per_step": el / args.steps * 1e6,
-                  "caller": "ebic_xgroup_evaluate (C ABI) on every rank, host buffers; "
-                            "cross-rank sum inside the count kernels"}
+        return {"value": n_sh / el, "unit": UNIT,
+                "h2d_bytes_per_step": int(sum((p + 1) * 8 + l * 2 for p, l in zip(pb, lb)) / nb),
+                "d2h_bytes_per_step": int(sum(16 * p for p in pb) / nb),
+                "us_per_step": el / args.steps * 1e6,
+                "caller": "ebic_xgroup_evaluate (C ABI) on every rank, host buffers; "
+                          "cross-rank sum inside the count kernels"}
 
-    big = None
-    if not sharded and not args.no_large:
-        ev.close()
-        big = large_roofline(args, peak)
+    e2e_sh = None
+    if sharded and xgroup is not None:
+        try:
+            e2e_sh = sharded_e2e()
+        except (RuntimeError, AssertionError) as exc:  # symmetric on every rank (shared results)
+            e2e_sh = {"error": f"in-kernel cross-rank path failed: {exc}"[:300]}
+
+    if xgroup is not None:  # the group refers to this context: release it first
+        if rank != 0:
+            _lib.check(_lib.lib.ebic_xgroup_destroy(xgroup))
+        dist.barrier()
+        if rank == 0:
+            _lib.check(_lib.lib.ebic_xgroup_destroy(xgroup))
+        xgroup = None
     cb = None
     if rank == 0 and not args.no_cpu_baseline:
         cb = cpu_reference(t, values, t.batches, steps=min(args.steps, 40), warmup=2,
@@ -645,12 +719,6 @@ def run_ours(args):
             "diag_back_to_back_us_per_step": b2b_us,
         }
         print(json.dumps(line), flush=True)
-    if xgroup is not None:
-        if rank != 0:
-            _lib.check(_lib.lib.ebic_xgroup_destroy(xgroup))
-        dist.barrier()
-        if rank == 0:
-            _lib.check(_lib.lib.ebic_xgroup_destroy(xgroup))
     ev.close()
     if sharded:
         dist.destroy_process_group()
