@@ -68,3 +68,14 @@ def test_reference_unit_tests_pass_on_dropin_gpu():
     rc, summary, out = _run(UNIT_DROPIN)
     assert rc == 0, out
     assert "test cases: 73" in summary and "failed: 0" in summary, summary
+
+
+DRAW_CHECK = oracle.HERE / "_ref" / "draw_check"
+
+
+@pytest.mark.skipif(not DRAW_CHECK.exists(), reason="oracle/_ref/draw_check not built")
+def test_shadow_bounded_draws_equal_reference_rng():
+    """detail::draw_index (cached reciprocal) == Rng::index (rng.hpp:20-32),
+    one million draws over a sweep of bounds, engine states equal after."""
+    rc, summary, out = _run(DRAW_CHECK)
+    assert rc == 0 and '"mismatches": 0' in summary, out
