@@ -5,6 +5,8 @@ Records the populations the reference GA hands to its top-rank list
 replays them through oracle/_ref/toprank_time_ref (reference evolution.hpp)
 and oracle/_ref/toprank_time_dropin (shadow evolution.hpp -> ebic_top_rank_update).
 Both print mean us/update and a digest of the final list (must agree).
+When tools/probes/build.sh has run, build_generation is timed on the same
+streams too (reference vs shadow headers, digest of the children).
 usage: python tools/toprank_compare.py > gpurun_out/toprank_compare.log
 """
 import json
@@ -33,6 +35,16 @@ with tempfile.TemporaryDirectory() as td:
             r = subprocess.run([str(oracle.HERE / "_ref" / f"toprank_time_{impl}"), str(path), "5"],
                                capture_output=True, text=True, check=True)
             out[impl] = json.loads(r.stdout)
+        bg = {}
+        for impl in ("ref", "dropin"):  # build_generation on the same stream (tools/probes/build.sh)
+            exe = ROOT / "tools" / "probes" / f"build_gen_compare_{impl}"
+            if exe.exists():
+                r = subprocess.run([str(exe), str(path)], capture_output=True, text=True, check=True)
+                bg[impl] = r.stdout.split()  # "build_generation us <t> digest <d>"
+        if len(bg) == 2:
+            print(json.dumps({"stream": name, "build_generation_reference_us": float(bg["ref"][2]),
+                              "build_generation_dropin_us": float(bg["dropin"][2]),
+                              "children_equal": bg["ref"][4] == bg["dropin"][4]}), flush=True)
         print(json.dumps({"stream": name, "updates": out["ref"]["updates"],
                           "reference_us_per_update": out["ref"]["us_per_update"],
                           "dropin_us_per_update": out["dropin"]["us_per_update"],
