@@ -381,3 +381,47 @@ def test_many_rows():
             got = ev.count_matches(pop, e)
             want = port.count_matches(v, pop.offsets, pop.col_indices, e)
             assert (got == want).all(), e
+
+
+@pytest.mark.parametrize("n_cols", [1400, 2047, 2048, 2049])
+def test_wide_matrix_layout_boundaries(n_cols):
+    """Around the widths where the staged tiles stop fitting shared memory
+    (1-plane rank rows of 32: ~1700 columns for two stages) and where the rank
+    layout is no longer built (2048 columns, 2C keys sorted per row): every
+    fallback (fp64 tile, direct kernel) stays exact."""
+    rng = np.random.default_rng(n_cols)
+    v = rng.standard_normal((700, n_cols))
+    v[:, 5] = v[:, 7]  # ties
+    pop = cbf(random_population(rng, n_cols, 300, max_len=9))
+    with eb.Evaluator(v) as ev:
+        for e in (0.0, 1e-9, 0.3):
+            got = ev.count_matches(pop, e)
+            assert (got == port.count_matches(v, pop.offsets, pop.col_indices, e)).all(), e
+
+
+def test_device_batch_limits():
+    """The device-pointer API takes up to 2048 series / 8192 columns per call
+    and rejects larger batches with the documented message."""
+    import torch
+    from paper_1801_03039_b200 import _lib
+    rng = np.random.default_rng(11)
+    v = rng.standard_normal((900, 64))
+    with eb.Evaluator(v) as ev:
+        for P in (2048, 2049):
+            series = [rng.choice(64, size=4, replace=False) for _ in range(P)]
+            pop = cbf(series)
+            d_off = torch.from_numpy(pop.offsets.astype(np.int64)).cuda()
+            d_cols = torch.from_numpy(pop.col_indices.astype(np.int16)).cuda()
+            d_cnt = torch.zeros(P, dtype=torch.int64, device="cuda")
+            st = torch.cuda.current_stream().cuda_stream
+            rc = _lib.lib.ebic_count_matches_device(ev.handle, d_off.data_ptr(), d_cols.data_ptr(), P,
+                                                    int(pop.offsets[-1]), 0.0, 0, d_cnt.data_ptr(), None, st)
+            if P == 2048:
+                _lib.check(rc)
+                torch.cuda.synchronize()
+                want = port.count_matches(v, pop.offsets, pop.col_indices, 0.0)
+                assert (d_cnt.cpu().numpy().astype(np.uint64) == want).all()
+            else:
+                assert rc != 0 and "2048 series" in _lib.lib.ebic_last_error().decode()
+            # the host path splits any size exactly
+            assert (ev.count_matches(pop, 0.0) == port.count_matches(v, pop.offsets, pop.col_indices, 0.0)).all()
