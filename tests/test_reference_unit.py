@@ -79,3 +79,27 @@ def test_shadow_bounded_draws_equal_reference_rng():
     one million draws over a sweep of bounds, engine states equal after."""
     rc, summary, out = _run(DRAW_CHECK)
     assert rc == 0 and '"mismatches": 0' in summary, out
+
+
+IO_REF = oracle.HERE / "_ref" / "io_check_ref"
+IO_DROPIN = oracle.HERE / "_ref" / "io_check_dropin"
+
+
+@pytest.mark.skipif(not (IO_REF.exists() and IO_DROPIN.exists()), reason="oracle/_ref/io_check_* not built")
+def test_result_files_byte_identical(tmp_path):
+    """include/ebic/io.hpp (result files written without a per-row JSON DOM)
+    against the reference io.hpp: result files (empty, no run summary, up to
+    ~200k rows per bicluster), truth and score files, read-back, plateau
+    thresholds, config parsing and error texts -- byte for byte."""
+    outs = {}
+    for name, exe in (("ref", IO_REF), ("dropin", IO_DROPIN)):
+        d = tmp_path / name
+        d.mkdir()
+        r = subprocess.run([str(exe), str(d)], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        files = {p.name: p.read_bytes() for p in sorted(d.iterdir())}
+        outs[name] = (r.stdout.replace(str(d), "<dir>"), files)
+    assert outs["ref"][0] == outs["dropin"][0]
+    assert outs["ref"][1].keys() == outs["dropin"][1].keys() and len(outs["ref"][1]) == 8
+    for k in outs["ref"][1]:
+        assert outs["ref"][1][k] == outs["dropin"][1][k], k

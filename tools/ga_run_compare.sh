@@ -17,5 +17,7 @@ run_pair() {  # name, args...
 }
 # BASELINE.json configs 0 and 3 at their stated iteration counts.
 run_pair c1 rows=500 cols=100 blocks=50x10,50x10,50x10 seed=1 population=600 iterations=1000 rng_seed=42 epsilon=1e-9 overlap_threshold=0.5 threshold=none
+# C4 shape with every top-rank entry written (threshold none): ~10^6 expanded rows in the output.
+run_pair c4_all rows=20000 cols=500 blocks=600x20,600x20,600x20,600x20,600x20 seed=2026 population=600 iterations=200 rng_seed=1 epsilon=1e-9 threshold=none
 run_pair c4 rows=20000 cols=500 blocks=600x20,600x20,600x20,600x20,600x20 seed=2026 population=600 iterations=5000 rng_seed=1 epsilon=1e-9
 cat $out
