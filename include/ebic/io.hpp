@@ -11,32 +11,116 @@
 // bytes are identical to the reference's `dump(2)`
 // (tests/test_reference_unit.py::test_result_files_byte_identical).
 
-#include <algorithm>
-#include <charconv>
-#include <cmath>
-#include <cstdint>
-#include <cstdio>
-#include <fstream>
-#include <map>
-#include <span>
-#include <stdexcept>
-#include <string>
-#include <string_view>
-#include <vector>
+#include "ebic/evolution.hpp"  // TopRankEntry (shadow)
+#include "ebic/expansion.hpp"  // resolve / expand (shadow, GPU)
+#include "ebic/metrics.hpp"    // CellRect, ScoreReport (reference)
 
 #include <json.hpp>
 
-#include "ebic/bicluster.hpp"
-#include "ebic/evolution.hpp"
-#include "ebic/expansion.hpp"
-#include "ebic/fitness.hpp"
-#include "ebic/matrix.hpp"
-#include "ebic/metrics.hpp"
+#include <algorithm>
+#include <charconv>
+#include <cmath>
+#include <fstream>
+#include <iterator>
+#include <map>
+#include <stdexcept>
+#include <string_view>
 
 namespace ebic {
+// :180-228 -- "key = value" lines ('#' starts a comment) or one flat JSON
+// object; later keys win.
+inline std::map<std::string, std::string> parse_config_text(const std::string& text) {
+    std::map<std::string, std::string> kv;
+    const std::size_t lead = text.find_first_not_of(" \t\r\n");
+    if (lead != std::string::npos && text[lead] == '{') {
+        const nlohmann::json doc = nlohmann::json::parse(text);
+        if (!doc.is_object()) throw std::runtime_error("config JSON must be an object");
+        for (const auto& [key, value] : doc.items()) kv[key] = value.is_string() ? value.get<std::string>() : value.dump();
+        return kv;
+    }
+    auto strip = [](std::string_view s, const char* blanks) {
+        const std::size_t b = s.find_first_not_of(blanks);
+        if (b == std::string_view::npos) return std::string();
+        return std::string(s.substr(b, s.find_last_not_of(blanks) - b + 1));
+    };
+    std::size_t number = 0;
+    for (std::size_t from = 0; from <= text.size();) {
+        std::size_t to = text.find('\n', from);
+        if (to == std::string::npos) to = text.size();
+        std::string_view raw(text.data() + from, to - from);
+        from = to + 1;
+        ++number;
+        raw = raw.substr(0, raw.find('#'));
+        const std::string line = strip(raw, " \t\r");
+        if (line.empty()) continue;
+        const std::size_t eq = line.find('=');
+        if (eq == std::string::npos)
+            throw std::runtime_error("config line " + std::to_string(number) + ": expected key = value");
+        std::string key = strip(std::string_view(line).substr(0, eq), " \t");
+        if (key.empty()) throw std::runtime_error("config line " + std::to_string(number) + ": empty key");
+        kv[std::move(key)] = strip(std::string_view(line).substr(eq + 1), " \t");
+    }
+    return kv;
+}
+
+inline std::map<std::string, std::string> load_config_file(const std::string& path) {
+    std::ifstream file(path);
+    if (!file) throw std::runtime_error("cannot read config file " + path);
+    const std::string text((std::istreambuf_iterator<char>(file)), std::istreambuf_iterator<char>());
+    return parse_config_text(text);
+}
+
+// :128-143 -- best Eq. 1 score a signal-free background sustains: a series
+// of length m keeps about n_rows / m! rows.
+inline double null_fitness_plateau(std::size_t n_rows, std::uint64_t sigma) {
+    const FitnessParams params{sigma};
+    double plateau = 0.0;
+    double m_factorial = 2.0;  // 2!
+    for (std::size_t m = 2; m <= 20; ++m) {
+        const auto rows = static_cast<std::uint64_t>(std::llround(static_cast<double>(n_rows) / m_factorial));
+        plateau = std::max(plateau, fitness_score(rows, m, params));
+        m_factorial *= static_cast<double>(m + 1);
+    }
+    return plateau;
+}
+
+
+// :145-162
+struct OutputOptions {
+    enum class Threshold : std::uint8_t { kAuto, kNone, kValue };
+    Threshold threshold = Threshold::kAuto;
+    double min_fitness = 0.0;
+    std::size_t max_biclusters = 100;
+};
+
+inline double resolve_min_fitness(const OutputOptions& opts, std::size_t n_rows, std::uint64_t sigma) {
+    if (opts.threshold == OutputOptions::Threshold::kAuto) return 2.0 * null_fitness_plateau(n_rows, sigma);
+    if (opts.threshold == OutputOptions::Threshold::kValue) return opts.min_fitness;
+    return 0.0;
+}
+
+
+// :164-178 -- threshold, cap, then exact rows and expansion per kept entry
+// (both on the GPU through this repo's expansion.hpp).
+inline std::vector<Bicluster> finalize_biclusters(std::span<const TopRankEntry> entries,
+                                                  const ExpressionMatrix& matrix,
+                                                  const ExpansionOptions& expansion, double epsilon,
+                                                  const OutputOptions& output, std::uint64_t sigma) {
+    const double floor = resolve_min_fitness(output, matrix.n_rows, sigma);
+    std::vector<Bicluster> kept;
+    for (const TopRankEntry& e : entries) {
+        if (kept.size() >= output.max_biclusters) break;
+        if (e.fitness < floor) continue;
+        kept.push_back(expand_bicluster(matrix, resolve_bicluster(matrix, e.series, e.fitness, epsilon),
+                                        expansion, epsilon));
+    }
+    return kept;
+}
+
 
 // :24-26 -- every number the tools write is rounded to six decimals.
 inline double round6(double x) { return std::round(x * 1e6) / 1e6; }
+
 
 // :28-42
 inline const char* row_flag_name(RowFlag f) {
@@ -53,6 +137,16 @@ inline RowFlag row_flag_from_name(const std::string& name) {
     throw std::runtime_error("unknown row flag: " + name);
 }
 
+
+// :57-62
+struct RunSummary {
+    std::size_t generations = 0;
+    std::uint64_t series_evaluated = 0;
+    std::uint64_t sigma = 0;
+    bool tabu_terminated = false;
+};
+
+
 // :44-55 -- one bicluster as a JSON object (keys sort as the library sorts).
 inline nlohmann::json bicluster_to_json(const Bicluster& b) {
     nlohmann::json cols = nlohmann::json::array();
@@ -67,13 +161,28 @@ inline nlohmann::json bicluster_to_json(const Bicluster& b) {
     return out;
 }
 
-// :57-62
-struct RunSummary {
-    std::size_t generations = 0;
-    std::uint64_t series_evaluated = 0;
-    std::uint64_t sigma = 0;
-    bool tabu_terminated = false;
-};
+
+// :109-126
+inline nlohmann::json score_to_json(const ScoreReport& report) {
+    auto rounded = [](const std::vector<double>& v) {
+        nlohmann::json a = nlohmann::json::array();
+        for (const double x : v) a.push_back(round6(x));
+        return a;
+    };
+    nlohmann::json out;
+    out["per_expected"] = rounded(report.per_expected);
+    out["per_found"] = rounded(report.per_found);
+    out["recovery"] = round6(report.recovery);
+    out["relevance"] = round6(report.relevance);
+    return out;
+}
+
+inline void write_score_file(const std::string& path, const ScoreReport& report) {
+    std::ofstream file(path);
+    if (!file) throw std::runtime_error("cannot write " + path);
+    file << score_to_json(report).dump(2) << '\n';
+}
+
 
 namespace detail {
 
@@ -139,6 +248,7 @@ inline std::string marker(const char* what, std::size_t i) {
 }
 
 }  // namespace detail
+
 
 // :64-78 -- {"biclusters": [...], "run": {...}} as `dump(2)` lays it out.
 // The library writes the document with a marker string in place of each
@@ -209,6 +319,7 @@ inline void write_biclusters_file(const std::string& path, std::span<const Biclu
     file.write(out.data(), static_cast<std::streamsize>(out.size()));
 }
 
+
 // :80-88
 inline void write_truth_file(const std::string& path, std::span<const CellRect> blocks) {
     nlohmann::json list = nlohmann::json::array();
@@ -219,6 +330,7 @@ inline void write_truth_file(const std::string& path, std::span<const CellRect> 
     if (!file) throw std::runtime_error("cannot write " + path);
     file << doc.dump(2) << '\n';
 }
+
 
 // :90-107 -- row/column sets of a results or ground-truth file (a bare
 // top-level array is accepted too).
@@ -235,115 +347,6 @@ inline std::vector<CellRect> read_rects_file(const std::string& path) {
         rects.push_back(make_rect(entry.at("rows").get<std::vector<std::size_t>>(),
                                   entry.at("columns").get<std::vector<std::size_t>>()));
     return rects;
-}
-
-// :109-126
-inline nlohmann::json score_to_json(const ScoreReport& report) {
-    auto rounded = [](const std::vector<double>& v) {
-        nlohmann::json a = nlohmann::json::array();
-        for (const double x : v) a.push_back(round6(x));
-        return a;
-    };
-    nlohmann::json out;
-    out["per_expected"] = rounded(report.per_expected);
-    out["per_found"] = rounded(report.per_found);
-    out["recovery"] = round6(report.recovery);
-    out["relevance"] = round6(report.relevance);
-    return out;
-}
-
-inline void write_score_file(const std::string& path, const ScoreReport& report) {
-    std::ofstream file(path);
-    if (!file) throw std::runtime_error("cannot write " + path);
-    file << score_to_json(report).dump(2) << '\n';
-}
-
-// :128-143 -- best Eq. 1 score a signal-free background sustains: a series
-// of length m keeps about n_rows / m! rows.
-inline double null_fitness_plateau(std::size_t n_rows, std::uint64_t sigma) {
-    const FitnessParams params{sigma};
-    double plateau = 0.0;
-    double m_factorial = 2.0;  // 2!
-    for (std::size_t m = 2; m <= 20; ++m) {
-        const auto rows = static_cast<std::uint64_t>(std::llround(static_cast<double>(n_rows) / m_factorial));
-        plateau = std::max(plateau, fitness_score(rows, m, params));
-        m_factorial *= static_cast<double>(m + 1);
-    }
-    return plateau;
-}
-
-// :145-162
-struct OutputOptions {
-    enum class Threshold : std::uint8_t { kAuto, kNone, kValue };
-    Threshold threshold = Threshold::kAuto;
-    double min_fitness = 0.0;
-    std::size_t max_biclusters = 100;
-};
-
-inline double resolve_min_fitness(const OutputOptions& opts, std::size_t n_rows, std::uint64_t sigma) {
-    if (opts.threshold == OutputOptions::Threshold::kAuto) return 2.0 * null_fitness_plateau(n_rows, sigma);
-    if (opts.threshold == OutputOptions::Threshold::kValue) return opts.min_fitness;
-    return 0.0;
-}
-
-// :164-178 -- threshold, cap, then exact rows and expansion per kept entry
-// (both on the GPU through this repo's expansion.hpp).
-inline std::vector<Bicluster> finalize_biclusters(std::span<const TopRankEntry> entries,
-                                                  const ExpressionMatrix& matrix,
-                                                  const ExpansionOptions& expansion, double epsilon,
-                                                  const OutputOptions& output, std::uint64_t sigma) {
-    const double floor = resolve_min_fitness(output, matrix.n_rows, sigma);
-    std::vector<Bicluster> kept;
-    for (const TopRankEntry& e : entries) {
-        if (kept.size() >= output.max_biclusters) break;
-        if (e.fitness < floor) continue;
-        kept.push_back(expand_bicluster(matrix, resolve_bicluster(matrix, e.series, e.fitness, epsilon),
-                                        expansion, epsilon));
-    }
-    return kept;
-}
-
-// :180-228 -- "key = value" lines ('#' starts a comment) or one flat JSON
-// object; later keys win.
-inline std::map<std::string, std::string> parse_config_text(const std::string& text) {
-    std::map<std::string, std::string> kv;
-    const std::size_t lead = text.find_first_not_of(" \t\r\n");
-    if (lead != std::string::npos && text[lead] == '{') {
-        const nlohmann::json doc = nlohmann::json::parse(text);
-        if (!doc.is_object()) throw std::runtime_error("config JSON must be an object");
-        for (const auto& [key, value] : doc.items()) kv[key] = value.is_string() ? value.get<std::string>() : value.dump();
-        return kv;
-    }
-    auto strip = [](std::string_view s, const char* blanks) {
-        const std::size_t b = s.find_first_not_of(blanks);
-        if (b == std::string_view::npos) return std::string();
-        return std::string(s.substr(b, s.find_last_not_of(blanks) - b + 1));
-    };
-    std::size_t number = 0;
-    for (std::size_t from = 0; from <= text.size();) {
-        std::size_t to = text.find('\n', from);
-        if (to == std::string::npos) to = text.size();
-        std::string_view raw(text.data() + from, to - from);
-        from = to + 1;
-        ++number;
-        raw = raw.substr(0, raw.find('#'));
-        const std::string line = strip(raw, " \t\r");
-        if (line.empty()) continue;
-        const std::size_t eq = line.find('=');
-        if (eq == std::string::npos)
-            throw std::runtime_error("config line " + std::to_string(number) + ": expected key = value");
-        std::string key = strip(std::string_view(line).substr(0, eq), " \t");
-        if (key.empty()) throw std::runtime_error("config line " + std::to_string(number) + ": empty key");
-        kv[std::move(key)] = strip(std::string_view(line).substr(eq + 1), " \t");
-    }
-    return kv;
-}
-
-inline std::map<std::string, std::string> load_config_file(const std::string& path) {
-    std::ifstream file(path);
-    if (!file) throw std::runtime_error("cannot read config file " + path);
-    const std::string text((std::istreambuf_iterator<char>(file)), std::istreambuf_iterator<char>());
-    return parse_config_text(text);
 }
 
 }  // namespace ebic
