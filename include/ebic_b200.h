@@ -5,7 +5,7 @@
  * seam: its evolutionary loop calls inline free functions.  Each entry point
  * below replaces one of those functions (cited as reference file:line, paths
  * relative to /root/reference/proj/include/ebic/).  The repo's shadowing
- * headers include/ebic/{fitness,expansion,evolution,io}.hpp bind these entry
+ * headers include/ebic/{fitness,expansion,evolution,io,synthgen}.hpp bind these entry
  * points behind the reference's own C++ signatures.
  *
  * Conventions
