@@ -47,6 +47,8 @@ inline GeneratedScenario generate(const ScenarioSpec& spec) {
         heights.push_back(shape.rows);
         widths.push_back(shape.cols);
     }
+    if (static_cast<int>(spec.pattern) > static_cast<int>(Pattern::kShiftScale))
+        return reference_generate(spec);  // out-of-range enum value: whatever the reference does
     Rng placement(spec.seed);  // the stream's first draws: rows, then columns
     const auto rows = detail::place_blocks(spec.n_rows, spec.overlap_rows, heights, placement);
     const auto cols = detail::place_blocks(spec.n_cols, spec.overlap_cols, widths, placement);
