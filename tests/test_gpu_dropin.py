@@ -47,6 +47,20 @@ CONFIGS = {
     "c3_noise_eps": ["rows=5000", "cols=200", "blocks=200x20,200x20,200x20", "noise=0.35", "seed=6",
                      "population=400", "iterations=60", "rng_seed=9", "epsilon=0.2",
                      "allow_negative=0"],
+    # every other generator pattern, eps = 0, wide tabu keys (> 256 columns),
+    # a narrow matrix that ends through the tabu list, another overlap threshold
+    "scale_eps0": ["rows=1500", "cols=120", "blocks=120x12,120x12", "pattern=scale", "seed=11",
+                   "population=500", "iterations=50", "rng_seed=4", "epsilon=0", "threshold=none"],
+    "shift_scale_wide": ["rows=2000", "cols=300", "blocks=150x15,150x15", "pattern=shift_scale",
+                         "seed=12", "population=600", "iterations=50", "rng_seed=5", "epsilon=1e-9",
+                         "threshold=none"],
+    "column_constant": ["rows=800", "cols=60", "blocks=80x8,80x8", "pattern=column_constant", "seed=13",
+                        "population=300", "iterations=40", "rng_seed=6", "epsilon=1e-9"],
+    "row_constant_overlap": ["rows=800", "cols=60", "blocks=80x8,80x8,80x8", "pattern=row_constant",
+                             "overlap=2", "seed=14", "population=300", "iterations=40", "rng_seed=7",
+                             "epsilon=1e-9", "overlap_threshold=0.3", "threshold=none"],
+    "narrow_tabu_end": ["rows=300", "cols=6", "blocks=30x3", "seed=15", "population=200",
+                        "iterations=400", "rng_seed=8", "epsilon=0", "threshold=none"],
 }
 
 
