@@ -114,6 +114,28 @@ def test_every_kernel_config_on_traces(cfg, name):
                 assert bits_equal(f, fit)
 
 
+# Scheduling, reduction and staging knobs (results must not depend on them).
+SCHEDULE_CONFIGS = [dict(EBIC_GRID="37"), dict(EBIC_GRID="300"), dict(EBIC_SCHED_STATIC="1"),
+                    dict(EBIC_MAX_PARTS="1"), dict(EBIC_REDUCE_TREE="1"), dict(EBIC_SLICE="64"),
+                    dict(EBIC_STAGES="2"), dict(EBIC_HOST_COPY="1"), dict(EBIC_GRAPH="0"),
+                    dict(EBIC_REDUCE_TREE="1", EBIC_GRID="37", EBIC_HOST_COPY="1")]
+
+
+@pytest.mark.parametrize("name", ["c4", "c3", "c1e"])
+@pytest.mark.parametrize("cfg", SCHEDULE_CONFIGS, ids=lambda d: "-".join(f"{k}={v}" for k, v in d.items()))
+def test_schedule_knobs_on_traces(cfg, name):
+    t = trace(name)
+    v = t.matrix()
+    with env(**cfg):
+        with eb.Evaluator(v) as ev:
+            for rep in range(2):  # the second pass reuses the graph / ring / tables
+                for off, cols, counts, fit in t.batches[:3]:
+                    f, c = ev.evaluate_population(eb.CbfPopulation(off, cols), eb.FitnessParams(t.sigma),
+                                                  t.eps, return_counts=True)
+                    assert (c == counts).all()
+                    assert bits_equal(f, fit)
+
+
 @pytest.mark.parametrize("cfg", KERNEL_CONFIGS[:8] + KERNEL_CONFIGS[10:11] + KERNEL_CONFIGS[-1:], ids=str)
 def test_edge_cases_vs_oracle(cfg):
     """Ragged row counts, ties, +-0, NaN/inf cells, odd eps values, len-1 series."""
