@@ -23,7 +23,11 @@ Arms
   --impl reference   the reference's own CPU implementation (oracle/_ref, the
                      unmodified headers compiled here) on all host threads.
 
-Multi-GPU (torchrun, one process per GPU): rows are sharded (64-row aligned);
+Multi-GPU: `bench.py --gpus N` re-executes itself under torch.distributed.run
+as N ranks when WORLD_SIZE is unset (the driver may also launch it with
+torchrun itself); a run whose WORLD_SIZE differs from --gpus is refused, and
+NCCL ranks need N visible GPUs (--backend gloo lets ranks share one GPU, for
+tests).  One process per GPU: rows are sharded (64-row aligned);
 each rank counts its shard.  `e2e` (host buffers, the public C ABI) sums
 across ranks inside the count kernels: every rank's final CTA adds into rank
 0's accumulator through CUDA IPC peer memory and the last one writes counts +
@@ -135,10 +139,22 @@ def algorithmic_bytes(rows: int, off: np.ndarray, cols: np.ndarray, cell_bytes: 
 
 
 # ---------------------------------------------------------------------------
-def cpu_reference(t, values, batches, steps, warmup, budget_s=60.0, threads=None):
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference(t, values, batches, steps, warmup, budget_s=60.0, threads=None, single_budget_s=None):
     """The reference CPU implementation on this host (oracle/_ref when built,
     else the C restatement).  Each step evaluates a bounded sample of a batch
-    (a prefix of its series) so the whole run stays within ~budget_s."""
+    (a prefix of its series) so the whole run stays within ~budget_s.
+    SURVEY.md §8(d): timed with T = nproc threads (`value`) and with T = 1
+    (`value_1t`, a smaller sample), after >= 2 s of multi-threaded warm-up."""
     import oracle
     threads = threads or os.cpu_count() or 1
     if oracle.REF_LIB.exists():
@@ -146,13 +162,13 @@ def cpu_reference(t, values, batches, steps, warmup, budget_s=60.0, threads=None
         m = ref.matrix(values)
         kind = "reference"
 
-        def run(off, cols):
-            return ref.evaluate_population(m, off, cols, t.sigma, t.eps, workers=threads)
+        def run(off, cols, workers):
+            return ref.evaluate_population(m, off, cols, t.sigma, t.eps, workers=workers)
     else:
         port = oracle.Port()
         kind, threads = "port", 1
 
-        def run(off, cols):
+        def run(off, cols, workers):
             return port.evaluate_population(values, off, cols, t.sigma, t.eps)[1]
 
     # Warm-up: >= 2 s of multi-threaded work (cold vCPUs).
@@ -161,46 +177,61 @@ def cpu_reference(t, values, batches, steps, warmup, budget_s=60.0, threads=None
     while time.perf_counter() - t0 < 2.0 or len(full) < max(1, warmup):
         off, cols, _, _ = batches[len(full) % len(batches)]
         a = time.perf_counter()
-        run(off, cols)
+        run(off, cols, threads)
         full.append((time.perf_counter() - a) / (len(off) - 1))
     per_series = min(full)
     P = len(batches[0][0]) - 1
-    sample = int(max(1, min(P, budget_s / max(steps, 1) / per_series)))
-    done = 0
-    t0 = time.perf_counter()
-    for k in range(steps):
-        off, cols, _, _ = batches[k % len(batches)]
-        n = min(sample, len(off) - 1)
-        sub_off = off[:n + 1]
-        run(sub_off, cols[:int(sub_off[-1])])
-        done += n
-    el = time.perf_counter() - t0
-    return {"value": done / el, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{steps} steps x first {sample} of {P} series of a C4 GA batch "
-                      f"(all {values.shape[0]} rows, eps={t.eps}); {threads} threads"}
+
+    def timed(workers, budget, per):
+        sample = int(max(1, min(P, budget / max(steps, 1) / per)))
+        done = 0
+        a = time.perf_counter()
+        for k in range(steps):
+            off, cols, _, _ = batches[k % len(batches)]
+            n = min(sample, len(off) - 1)
+            sub_off = off[:n + 1]
+            run(sub_off, cols[:int(sub_off[-1])], workers)
+            done += n
+        return done / (time.perf_counter() - a), sample
+
+    value, sample = timed(threads, budget_s, per_series)
+    out = {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+           "sample": f"{steps} steps x first {sample} of {P} series of a {t.name.upper()} GA batch "
+                     f"(all {values.shape[0]} rows, eps={t.eps}); {threads} threads",
+           "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    if single_budget_s and threads > 1:
+        # one thread is ~threads x slower per series: scale the estimate
+        v1, s1 = timed(1, single_budget_s, per_series * threads)
+        out["value_1t"] = v1
+        out["sample_1t"] = f"{steps} steps x first {s1} series, 1 thread"
+    return out
 
 
 # ---------------------------------------------------------------------------
 def run_reference_arm(args):
+    """The reference's own CPU implementation (oracle/_ref) on all host
+    threads, on the same workload.  Nothing from the product package is
+    loaded: the input matrix comes from the reference's `ebic::generate`."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     t = load_workload(args.workload)
-    values = t.matrix()
-    cb = cpu_reference(t, values, t.batches, args.steps, args.warmup)
+    values = t.matrix_reference()
+    cb = cpu_reference(t, values, t.batches, args.steps, args.warmup,
+                       single_budget_s=min(20.0, args.cpu_budget))
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(t, args),
+        "config": workload_config(t, args, args.gpus, args.gpus),
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(t, args):
+def workload_config(t, args, world=1, devices=1):
     s = t.spec
     return {"workload": f"{args.workload}: synthetic {s['rows']}x{s['cols']} "
                         f"({len(s['blocks'])} planted {s['blocks'][0][0]}x{s['blocks'][0][1]} trend blocks, "
@@ -208,8 +239,8 @@ def workload_config(t, args):
             "rows": s["rows"], "cols": s["cols"],
             "series_per_step": round(float(np.mean([len(b[0]) - 1 for b in t.batches])), 1),
             "eps": t.eps, "sigma": t.sigma, "l2": "evicted between timed steps (512 MB read, outside the timed events)",
-            "parallelism": f"rows sharded over {args.gpus} GPU(s)"
-                           + ("" if args.gpus == 1 and not args.force_sharded else
+            "parallelism": f"rows sharded over {world} rank(s) on {devices} GPU(s)"
+                           + ("" if world == 1 and not args.force_sharded else
                               ("; value: cross-rank sum inside the count kernels (CUDA IPC peer memory)"
                                if args.reduce == "kernel" else "; value: NCCL all-reduce of counts")
                               + "; e2e: cross-rank sum inside the count kernels")}
@@ -373,12 +404,25 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    n_visible = torch.cuda.device_count()
+    if world != args.gpus:
+        # a line whose rank count differs from --gpus would mislabel the run
+        print(f"[bench] refusing to run: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
+    if args.backend == "nccl" and world > n_visible:
+        print(f"[bench] refusing to run: {world} NCCL ranks need {world} GPUs, {n_visible} visible "
+              f"(--backend gloo lets ranks share a GPU)", file=sys.stderr)
+        sys.exit(2)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, n_visible)
+    n_devices = min(world, max(1, n_visible))
     sharded = world > 1 or args.force_sharded
     if sharded:
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
+        # communicator size and transport (NVLink / NVLS) in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         if args.backend == "nccl":
             dist.init_process_group("nccl", rank=rank, world_size=world,
                                     device_id=torch.device("cuda", local))
@@ -489,7 +533,6 @@ def run_ours(args):
     layout = ev.info().layout
     for b, (off, cols, _, _) in zip(dev_batches, t.batches):
         b["bytes"] = algorithmic_bytes(hi - lo, off, cols, LAYOUT_CELL_BYTES[layout])
-        b["bytes_f64"] = algorithmic_bytes(hi - lo, off, cols, 8)
     for b in dev_batches:
         step(b)
         torch.cuda.synchronize()
@@ -512,7 +555,6 @@ def run_ours(args):
     torch.cuda.synchronize()
     series = 0
     nbytes = 0
-    nbytes_f64 = 0
     for k in range(args.steps):
         b = dev_batches[k % len(dev_batches)]
         evict_l2()                          # evict L2 (outside the events)
@@ -522,7 +564,6 @@ def run_ours(args):
         ends[k].record(stream)
         series += b["P"]
         nbytes += b["bytes"]
-        nbytes_f64 += b["bytes_f64"]
     torch.cuda.synchronize()
     if sharded:
         dist.barrier()
@@ -671,7 +712,7 @@ def run_ours(args):
     cb = None
     if rank == 0 and not args.no_cpu_baseline:
         cb = cpu_reference(t, values, t.batches, steps=min(args.steps, 40), warmup=2,
-                           budget_s=args.cpu_budget)
+                           budget_s=args.cpu_budget, single_budget_s=min(10.0, args.cpu_budget))
 
     if rank == 0:
         avg_bytes = nbytes / args.steps
@@ -686,7 +727,6 @@ def run_ours(args):
                     "frac": achieved / peak, "traffic": traffic,
                     "algorithmic_bytes_per_launch": avg_bytes,
                     "layout": LAYOUT_NAMES[layout], "cell_bytes": LAYOUT_CELL_BYTES[layout],
-                    "fp64_equivalent_GBps": nbytes_f64 / args.steps / (avg_launch_ms / 1e3) / 1e9,
                     "peak_source": peak_src,
                     "kernel": "count_tma_kernel (fused Eq. 1 epilogue)",
                     "avg_launch_us": avg_launch_ms * 1e3}
@@ -695,7 +735,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator, bit-identical) + reference GA batches",
-            "config": workload_config(t, args),
+            "config": workload_config(t, args, world, n_devices),
             "roofline": roof, "cpu_baseline": cb, "clocks": clk,
             "e2e": e2e_sh if sharded else ({"value": e2e_cpp["e2e_biclusters_per_s"], "unit": UNIT,
                      "h2d_bytes_per_step": e2e_cpp["h2d_bytes_per_step"],
@@ -724,6 +764,20 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` started without torchrun: re-executes itself as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1 and
+    returns the launcher's exit code.  Rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -748,6 +802,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     if args.impl == "reference":
         run_reference_arm(args)
     else:

@@ -18,6 +18,13 @@
  *  - Host buffers are caller-owned; the context owns every device copy.
  *  - A context is not thread-safe: calls on one context must be serialised
  *    (the reference evaluates one batch at a time, parallel.hpp:14-16).
+ *    Device-pointer calls may use different streams: a launch on a stream
+ *    other than the previous launch's first waits (on the device) for work
+ *    already queued on that stream, since launches share the context's
+ *    scratch.  The host-buffer calls use the context's own stream.
+ *  - The matrix is copied into device memory when the context is created;
+ *    later changes to the caller's host buffer are not seen (create a new
+ *    context for a new matrix, as the drop-in headers do per run).
  *  - The population travels in CBF form exactly as the reference builds it
  *    (cbf.hpp:43-52): offsets[P+1] (size_t, offsets[0] == 0) and the
  *    concatenated uint16 column indices.

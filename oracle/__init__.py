@@ -234,6 +234,9 @@ class Ref:
         L.ref_run_trace.restype = C.c_long
         L.ref_run_trace.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, C.c_uint64, C.c_double,
                                     C.c_uint64, C.c_uint, C.c_size_t, C.c_char_p]
+        L.ref_run_trace_sel.restype = C.c_long
+        L.ref_run_trace_sel.argtypes = [C.c_void_p, C.c_size_t, C.c_size_t, C.c_uint64, C.c_double,
+                                        C.c_uint64, C.c_uint, C.c_size_t, C.c_size_t, C.c_char_p]
         self.lib = L
 
     class Matrix:
@@ -313,6 +316,14 @@ class Ref:
             raise RuntimeError("reference run failed")
         return n
 
+
+    def run_trace_sel(self, m, path, population=600, iterations=10, rng_seed=1, eps=0.0, sigma=0,
+                      threads=1, record_first=0, record_every=0):
+        n = self.lib.ref_run_trace_sel(m.h, population, iterations, rng_seed, float(eps), sigma,
+                                       threads, record_first, record_every, str(path).encode())
+        if n < 0:
+            raise RuntimeError("reference run failed")
+        return n
 
     class TopRank:
         """The reference's own TopRankList (evolution.hpp:142-218)."""
@@ -400,4 +411,19 @@ def read_trace(path):
         cols = np.frombuffer(data, np.uint16, L, at).copy(); at += 2 * L
         counts = np.frombuffer(data, np.uint64, P, at).copy(); at += 8 * P
         out.append((off, cols, counts))
+    return out
+
+
+def read_trace_sel(path):
+    """Parse a ref_run_trace_sel file -> list of (batch index, offsets, cols, counts)."""
+    data = Path(path).read_bytes()
+    at, out = 0, []
+    while at < len(data):
+        k = int(np.frombuffer(data, np.uint64, 1, at)[0]); at += 8
+        P = int(np.frombuffer(data, np.uint64, 1, at)[0]); at += 8
+        off = np.frombuffer(data, np.uint64, P + 1, at).copy(); at += 8 * (P + 1)
+        L = int(off[-1])
+        cols = np.frombuffer(data, np.uint16, L, at).copy(); at += 2 * L
+        counts = np.frombuffer(data, np.uint64, P, at).copy(); at += 8 * P
+        out.append((k, off, cols, counts))
     return out

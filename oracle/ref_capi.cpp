@@ -181,6 +181,52 @@ long ref_run_trace(void* h, std::size_t population, std::size_t iterations, std:
 }
 
 
+// Same run, recording only selected batches: batch k (k = 0 is the initial
+// population, k = g the novel children of generation g) is recorded iff
+// k < record_first or (record_every && k % record_every == 0) -- early
+// generations plus a sparse sample of the steady state up to `iterations`.
+// Layout: repeated { u64 k; u64 P; u64 offsets[P+1]; u16 cols[]; u64 counts[P] }.
+long ref_run_trace_sel(void* h, std::size_t population, std::size_t iterations, std::uint64_t rng_seed,
+                       double eps, std::uint64_t sigma, unsigned threads, std::size_t record_first,
+                       std::size_t record_every, const char* path) {
+    const auto& m = *static_cast<ExpressionMatrix*>(h);
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) return -1;
+    RunConfig cfg;
+    cfg.evo.population_size = population;
+    cfg.evo.max_iterations = iterations;
+    cfg.evo.rng_seed = rng_seed;
+    cfg.epsilon = eps;
+    cfg.sigma = sigma;
+    cfg.threads = threads;
+    const ChunkPlan plan = make_chunk_plan(m.n_rows, threads);
+    long recorded = 0;
+    std::uint64_t k = 0;
+    RunHooks hooks;
+    hooks.on_evaluate = [&](std::span<const ColumnSeries> novel) {
+        const std::uint64_t batch = k++;
+        if (!(batch < record_first || (record_every && batch % record_every == 0))) return;
+        const CbfPopulation cbf = encode_population(novel);
+        const auto counts = count_matches(m, cbf, plan, eps);
+        const std::uint64_t p = cbf.size();
+        std::fwrite(&batch, sizeof batch, 1, f);
+        std::fwrite(&p, sizeof p, 1, f);
+        std::vector<std::uint64_t> off(cbf.offsets.begin(), cbf.offsets.end());
+        std::fwrite(off.data(), sizeof(std::uint64_t), off.size(), f);
+        std::fwrite(cbf.col_indices.data(), sizeof(std::uint16_t), cbf.col_indices.size(), f);
+        std::fwrite(counts.data(), sizeof(std::uint64_t), counts.size(), f);
+        ++recorded;
+    };
+    try {
+        (void)run(m, cfg, hooks);
+    } catch (...) {
+        std::fclose(f);
+        return -1;
+    }
+    std::fclose(f);
+    return recorded;
+}
+
 // ---- fixture generators: the input streams of the reference's own tests ----
 
 // proj/tests/acceptance_main.cpp:233-251 (property_match_counts): a 300x30

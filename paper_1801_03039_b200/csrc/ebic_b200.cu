@@ -24,7 +24,11 @@
 #include <memory>
 #include <mutex>
 #include <atomic>
+#include <condition_variable>
+#include <exception>
+#include <functional>
 #include <map>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -90,7 +94,7 @@ int env_int(const char* name, int dflt) {
 // context is created so the per-generation launch path makes no getenv calls.
 struct Knobs {
     int force_direct, rpg, rpl, stages, ncw, slice, layout_f64, no_collapse, sched_static,
-        max_parts, reduce_tree, grid, phase_timing, spg, host_copy, xshard, graph;
+        max_parts, reduce_tree, grid, phase_timing, spg, host_copy, xshard, graph, debug_mode;
     static Knobs from_env() {
         Knobs k;
         k.force_direct = env_int("EBIC_FORCE_DIRECT", 0);
@@ -110,6 +114,7 @@ struct Knobs {
         k.host_copy = env_int("EBIC_HOST_COPY", 0);
         k.xshard = env_int("EBIC_XSHARD", 1);  // in-kernel cross-shard reduction
         k.graph = env_int("EBIC_GRAPH", 1);    // count launches through a cached one-node graph
+        k.debug_mode = env_int("EBIC_DEBUG_MODE", 0);  // measurement only: wrong results
         return k;
     }
 };
@@ -224,6 +229,12 @@ struct Shard {
     double host_us[5] = {0, 0, 0, 0, 0};
     uint64_t host_calls = 0;
     int last_reduce = -1;  // reduction-tail mode of the last launch
+    // Stream of the previous count launch.  Launches share this shard's
+    // scratch (striped accumulators, tickets, Eq. 1 tables), so a launch on
+    // another stream (device API on a caller's stream vs the host API on
+    // `stream`) first waits for everything already queued on the previous one.
+    cudaStream_t cur_stream = nullptr;
+    cudaEvent_t switch_event = nullptr;
     bool last_collapsed = false;
     // choose_config memo (same P / L / layout as the previous launch)
     size_t memo_P = 0, memo_L = 0;
@@ -282,6 +293,8 @@ void ensure_partial(Shard& s, size_t P, int grid, bool striped) {
     const size_t need = striped ? P * kStripes : (size_t(grid) + (grid + gsz - 1) / gsz) * P;
     const int mode = striped ? 1 : 0;
     if (need <= s.partial_cap && mode == s.last_reduce) return;
+    // a launch still queued on the previous stream may use the old scratch
+    if (s.cur_stream) CK(cudaStreamSynchronize(s.cur_stream));
     s.last_reduce = mode;
     if (need <= s.partial_cap) {  // mode switch: the tree leaves non-zero rows behind
         CK(cudaMemsetAsync(s.d_partial, 0, s.partial_cap * sizeof(uint32_t), s.stream));
@@ -300,6 +313,97 @@ void ensure_partial(Shard& s, size_t P, int grid, bool striped) {
 
 }  // namespace
 
+// One host thread per extra row shard: the per-generation work of shard i
+// (CBF staging + count launch) runs on its own thread with its device
+// current, concurrently with the other shards, instead of a serial
+// cudaSetDevice + launch loop on the caller's thread (the reference runs all
+// row chunks at once on its ThreadPool, parallel.hpp:40-55).  Shard 0 runs on
+// the caller's thread.  Workers spin on the job counter for EBIC_SPIN_US
+// (default 2000 us: the GA's host work between generations) before
+// sleeping, so a hand-off costs ~0.1-0.3 us instead of a futex wake.
+class ShardPool {
+  public:
+    ShardPool(const std::vector<int>& devices, int spin_us) : spin_us_(spin_us) {
+        const size_t n = devices.size();
+        done_ = std::make_unique<std::atomic<uint64_t>[]>(n);
+        errors_.resize(n);
+        for (size_t i = 1; i < n; ++i) {
+            done_[i].store(0);
+            threads_.emplace_back([this, i, dev = devices[i]] { loop(i, dev); });
+        }
+    }
+    ~ShardPool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_.store(true, std::memory_order_release);
+        }
+        cv_.notify_all();
+        for (std::thread& t : threads_) t.join();
+    }
+    // Runs f(i) for every shard i (i >= 1 on the workers, 0 here) and
+    // returns when all are done; the first exception is rethrown.
+    void run(const std::function<void(size_t)>& f) {
+        job_ = &f;
+        for (auto& e : errors_) e = nullptr;
+        uint64_t s;
+        {
+            std::lock_guard<std::mutex> lk(m_);  // pairs with the sleepers' predicate check
+            s = seq_.fetch_add(1, std::memory_order_acq_rel) + 1;
+        }
+        cv_.notify_all();
+        try {
+            f(0);
+        } catch (...) {
+            errors_[0] = std::current_exception();
+        }
+        for (size_t i = 1; i <= threads_.size(); ++i)
+            while (done_[i].load(std::memory_order_acquire) != s) {
+            }
+        job_ = nullptr;
+        for (auto& e : errors_)
+            if (e) std::rethrow_exception(e);
+    }
+
+  private:
+    void loop(size_t i, int dev) {
+        cudaSetDevice(dev);
+        uint64_t seen = 0;
+        for (;;) {
+            const auto t0 = std::chrono::steady_clock::now();
+            uint64_t s = seen;
+            for (uint32_t k = 0;; ++k) {
+                s = seq_.load(std::memory_order_acquire);
+                if (s != seen || stop_.load(std::memory_order_acquire)) break;
+                if ((k & 255) == 255 &&
+                    std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(spin_us_)) {
+                    std::unique_lock<std::mutex> lk(m_);
+                    cv_.wait(lk, [&] {
+                        return seq_.load(std::memory_order_acquire) != seen ||
+                               stop_.load(std::memory_order_acquire);
+                    });
+                }
+            }
+            if (stop_.load(std::memory_order_acquire)) return;
+            seen = s;
+            try {
+                (*job_)(i);
+            } catch (...) {
+                errors_[i] = std::current_exception();
+            }
+            done_[i].store(s, std::memory_order_release);
+        }
+    }
+    int spin_us_;
+    std::vector<std::thread> threads_;
+    std::unique_ptr<std::atomic<uint64_t>[]> done_;
+    std::vector<std::exception_ptr> errors_;
+    const std::function<void(size_t)>* job_ = nullptr;
+    std::atomic<uint64_t> seq_{0};
+    std::atomic<bool> stop_{false};
+    std::mutex m_;
+    std::condition_variable cv_;
+};
+
 struct ebic_ctx {
     size_t n_rows = 0;      // rows held
     size_t n_cols = 0;
@@ -312,6 +416,24 @@ struct ebic_ctx {
     unsigned long long* d_xacc = nullptr;
     size_t xacc_cap = 0;
     unsigned int* d_xticket = nullptr;
+    std::unique_ptr<ShardPool> pool;  // several shards: one launch thread per extra shard
+    // Runs f(shard) for every shard, concurrently when there are several.
+    void for_shards(const std::function<void(Shard&)>& f) {
+        if (shards.size() == 1) {
+            DeviceGuard g(shards[0].device);
+            f(shards[0]);
+            return;
+        }
+        if (!pool) {
+            std::vector<int> devs;
+            for (const Shard& s : shards) devs.push_back(s.device);
+            pool = std::make_unique<ShardPool>(devs, env_int("EBIC_SPIN_US", 2000));
+        }
+        pool->run([&](size_t i) {
+            DeviceGuard g(shards[i].device);
+            f(shards[i]);
+        });
+    }
 };
 
 namespace {
@@ -518,12 +640,17 @@ void launch_tma_t(const CUtensorMap& tm, const CountParams& p, int grid, size_t 
     auto k = count_tma_kernel<W, NCW>;
     // The attribute is per function and device; set it only when it grows so
     // the per-generation launch path makes no extra driver calls.
-    static int smem_set[64] = {0};
+    // (atomic: the shards of one context launch from their own host threads)
+    static std::atomic<int> smem_set[64] = {};
     int dev = sh ? sh->device : 0;  // the caller's DeviceGuard made it current
     if (!sh) CK(cudaGetDevice(&dev));
-    if (dev < 0 || dev >= 64 || (int)smem > smem_set[dev]) {
+    if (dev < 0 || dev >= 64 || (int)smem > smem_set[dev].load(std::memory_order_acquire)) {
         CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        if (dev >= 0 && dev < 64) smem_set[dev] = (int)smem;
+        if (dev >= 0 && dev < 64) {
+            int cur = smem_set[dev].load(std::memory_order_relaxed);
+            while ((int)smem > cur && !smem_set[dev].compare_exchange_weak(cur, (int)smem)) {
+            }
+        }
     }
     void* args[2] = {const_cast<CUtensorMap*>(&tm), const_cast<CountParams*>(&p)};
     launch_kernel(sh, reinterpret_cast<const void*>(k), grid, (NCW + 1) * 32, smem, st, args);
@@ -728,6 +855,8 @@ const Tables& ensure_tables(Shard& s, uint64_t sigma, size_t total_rows) {
     Tables& t = s.tables;
     if (t.d_log && t.sigma == sigma && t.n == total_rows + 1) return t;
     DeviceGuard g(s.device);
+    // a launch still queued on the previous stream may read the old tables
+    if (s.cur_stream) CK(cudaStreamSynchronize(s.cur_stream));
     const size_t n = total_rows + 1;
     std::vector<double> lg(n, 0.0), ex(n, 1.0);
     for (size_t c = 2; c < n; ++c) lg[c] = std::log(static_cast<double>(c - 1));
@@ -758,6 +887,12 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
     if (P == 0) return;
     if (P > 0xffffffffull || L > 0xffffffffull || s.rows > 0xffffffffull)
         fail(EBIC_ERR_INVALID_ARGUMENT, "population or shard too large for one launch");
+    if (s.cur_stream != st) {
+        if (!s.switch_event) CK(cudaEventCreateWithFlags(&s.switch_event, cudaEventDisableTiming));
+        CK(cudaEventRecord(s.switch_event, s.cur_stream ? s.cur_stream : s.stream));
+        CK(cudaStreamWaitEvent(st, s.switch_event, 0));
+        s.cur_stream = st;
+    }
     CountParams p{};
     p.offsets = d_off;
     p.cols = d_cols;
@@ -789,6 +924,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         p.cbf_seq = (unsigned int)++s.cbf_seq;
     }
     p.phase_ns = s.d_phase;
+    p.debug_mode = (uint32_t)s.knobs.debug_mode;
     if (d_fit) {
         const Tables& t = ensure_tables(s, sigma, ctx.total_rows);
         p.logt = t.d_log;
@@ -995,8 +1131,8 @@ void host_evaluate_xshard(ebic_ctx& ctx, const size_t* off, const uint16_t* cols
         (void)cudaGetLastError();
     };
     try {
-    for (Shard& s : ctx.shards) {
-        DeviceGuard g(s.device);
+    // every shard stages and launches on its own host thread (ShardPool)
+    ctx.for_shards([&](Shard& s) {
         const StagedCbf in = stage_cbf(s, off, cols, P);
         if (s.knobs.host_copy)
             CK(cudaMemcpyAsync(s.d_in, s.h_in_map, in.bytes, cudaMemcpyHostToDevice, s.stream));
@@ -1008,7 +1144,7 @@ void host_evaluate_xshard(ebic_ctx& ctx, const size_t* off, const uint16_t* cols
                      s.knobs.host_copy ? nullptr : s.h_in_map, in.bytes, ctx.d_xacc, ctx.d_xticket,
                      static_cast<uint32_t>(ctx.shards.size()));
         if (&s == &s0) s0.host_us[2] += us_since(tp);
-    }
+    });
     volatile unsigned long long* flag = reinterpret_cast<volatile unsigned long long*>(s0.h_map);
     for (uint64_t spin = 0;; ++spin) {
         if (*flag == seq) break;
@@ -1050,8 +1186,7 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
         host_evaluate_xshard(ctx, off, cols, P, L, eps, want_fit, sigma, counts_out, fit_out, tp);
         return;
     }
-    for (Shard& s : ctx.shards) {
-        DeviceGuard g(s.device);
+    ctx.for_shards([&](Shard& s) {
         grow_mapped(&s.h_map, &s.h_map_cap, 128 + P * 16);
         // A single TMA launch copies the staged CBF to the device itself (CTA
         // 0, stage_host_cbf): no cudaMemcpyAsync on the per-generation path.
@@ -1084,7 +1219,7 @@ void host_evaluate(ebic_ctx& ctx, const size_t* off, const uint16_t* cols, size_
             a = b;
         }
         if (&s == &s0) s0.host_us[2] += us_since(tp);
-    }
+    });
     std::vector<uint64_t> total;
     if (!single) total.assign(P, 0);
     for (Shard& s : ctx.shards) {
@@ -1185,6 +1320,7 @@ void free_shard(Shard& s) {
         cudaFree(rl.d_excl_vals);
     }
     cudaFree(s.d_phase);
+    if (s.switch_event) cudaEventDestroy(s.switch_event);
     if (s.stream) cudaStreamDestroy(s.stream);
 }
 
@@ -1281,6 +1417,7 @@ struct ebic_xgroup {
     unsigned char* d_base = nullptr;  // accumulator allocation (own or IPC-opened)
     unsigned char* shm = nullptr;     // mapped result block
     unsigned char* dev_shm = nullptr; // its device address
+    cudaStream_t launch_stream = nullptr;  // stream of the last launch (polled while waiting)
     size_t shm_bytes = 0;
     std::string shm_name;
     unsigned long long last_seq = 0;
@@ -1360,6 +1497,7 @@ int ebic_ctx_create_shard_device(const double* d_row_major, size_t shard_rows, s
 int ebic_ctx_destroy(ebic_ctx* ctx) {
     return guarded([&] {
         if (!ctx) return;
+        ctx->pool.reset();  // join the launch threads before their shards go away
         for (Shard& s : ctx->shards) free_shard(s);
         if (ctx->d_xacc || ctx->d_xticket) {
             cudaSetDevice(ctx->shards[0].device);
@@ -1701,6 +1839,7 @@ void xgroup_launch(ebic_xgroup* g, const uint64_t* d_off, const uint16_t* d_cols
     launch_count(ctx, s, d_off, d_cols, P, L, eps, counts, fit, sigma, st, 0,
                  reinterpret_cast<unsigned long long*>(dev_shm), seq, host_cbf, cbf_bytes, acc, ticket,
                  static_cast<uint32_t>(g->n_ranks));
+    g->launch_stream = st;
 }
 
 void xgroup_wait(ebic_xgroup* g, uint64_t seq, size_t P, uint64_t* counts_out, double* fit_out,
@@ -1743,7 +1882,10 @@ int ebic_xgroup_wait(ebic_xgroup* g, uint64_t seq, size_t n_series, uint64_t* co
     return guarded([&] {
         if (!g) fail(EBIC_ERR_INVALID_ARGUMENT, "null group");
         if (n_series > g->max_series) fail(EBIC_ERR_INVALID_ARGUMENT, "n_series above max_series");
-        xgroup_wait(g, seq, n_series, counts_out, fitness_out, g->ctx->shards[0].stream);
+        // poll the stream the count kernel was launched on, so a failed
+        // launch surfaces at once instead of after the timeout
+        xgroup_wait(g, seq, n_series, counts_out, fitness_out,
+                    g->launch_stream ? g->launch_stream : g->ctx->shards[0].stream);
     });
 }
 

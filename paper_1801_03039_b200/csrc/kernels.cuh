@@ -190,6 +190,10 @@ struct CountParams {
     unsigned int* __restrict__ xticket;
     uint32_t n_xshards;
     unsigned long long* __restrict__ phase_ns;  // optional [grid][8] %globaltimer stamps
+    // Measurement only (EBIC_DEBUG_MODE; results are wrong): 1 = consumers
+    // skip the walk (pure TMA streaming time), 2 = the producer skips the
+    // loads (pure walk time over stale stages).
+    uint32_t debug_mode;
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -1079,12 +1083,16 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                 if (p.scratch_in_stage && issued == p.stages - 1) mbar_wait(prol_bar, 0);
                 mbar_wait(&empty_bar[st], phase ^ 1u);
                 s_next[st] = 0;  // published to the consumers by the arrive below (release)
-                mbar_arrive_expect_tx(&full_bar[st], p.stage_bytes);
-                unsigned char* dst = stage_base + size_t(st) * p.stage_bytes;
-                for (uint32_t b = 0; b < p.n_boxes; ++b)
-                    tma_load_2d(dst + size_t(b) * p.box_cols * Walker::kColBytes, &tmap,
-                                &full_bar[st], static_cast<int>(tile * Walker::kDim0PerTile),
-                                static_cast<int>(b * p.box_cols));
+                if (p.debug_mode == 2) {
+                    mbar_arrive(&full_bar[st]);
+                } else {
+                    mbar_arrive_expect_tx(&full_bar[st], p.stage_bytes);
+                    unsigned char* dst = stage_base + size_t(st) * p.stage_bytes;
+                    for (uint32_t b = 0; b < p.n_boxes; ++b)
+                        tma_load_2d(dst + size_t(b) * p.box_cols * Walker::kColBytes, &tmap,
+                                    &full_bar[st], static_cast<int>(tile * Walker::kDim0PerTile),
+                                    static_cast<int>(b * p.box_cols));
+                }
                 if (++st == p.stages) st = 0, phase ^= 1u;
             }
         }
@@ -1161,7 +1169,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                 if (lane == 0) v = atomicAdd(&s_next[st], 1u);
                 return __shfl_sync(0xffffffffu, v, 0);
             };
-            uint32_t k = grab();
+            uint32_t k = p.debug_mode == 1 ? n_here : grab();
             while (k < n_here) {
                 const uint32_t ch = c_hi - 1 - k;
                 k = grab();

@@ -69,19 +69,21 @@ class RowShardedEvaluator:
         rows = values if is_shard else values[self.lo:self.hi]
         if rows.shape[0] != self.hi - self.lo:
             raise ValueError("shard rows do not match shard_range")
+        if reduce not in ("kernel", "collective"):
+            raise ValueError("reduce must be 'kernel' or 'collective'")
         self.rows = np.ascontiguousarray(rows, dtype=np.float64)
         self._ev = None
         self._xg = None
+        self._device = device
         self._seq = 0
         self.max_series = int(max_series)
         if local_counter is None:
             dev = device if device is not None else 0
+            self._device = dev
             self._ev = Evaluator(self.rows, devices=[dev], shard=(self.lo, total))
             local_counter = self._ev.count_matches
             if reduce == "kernel":
                 self._join_group()
-        elif reduce not in ("kernel", "collective"):
-            raise ValueError("reduce must be 'kernel' or 'collective'")
         self.reduce = "kernel" if self._xg is not None else "collective"
         self._local = local_counter
 
@@ -105,7 +107,7 @@ class RowShardedEvaluator:
                                           self.max_series, C.byref(g)) == 0)
         backend = self.dist.get_backend(self.group)
         agree = torch.tensor([ok], dtype=torch.int32,
-                             device="cuda" if backend == "nccl" else "cpu")
+                             device=torch.device("cuda", self._device) if backend == "nccl" else "cpu")
         self.dist.all_reduce(agree, op=self.dist.ReduceOp.MIN, group=self.group)
         if int(agree.item()):
             self._xg = g
@@ -160,6 +162,14 @@ class RowShardedEvaluator:
         import torch
         part = np.asarray(self._local(pop, epsilon), dtype=np.uint64)
         t = torch.from_numpy(part.astype(np.int64))
+        if self.dist.get_backend(self.group) == "nccl":
+            # NCCL reduces device tensors only: the partials go through this
+            # rank's GPU (int64 sums are exact on any backend)
+            dev = torch.device("cuda", self._device if self._device is not None
+                               else torch.cuda.current_device())
+            td = t.to(dev)
+            self.dist.all_reduce(td, op=self.dist.ReduceOp.SUM, group=self.group)
+            return td.cpu().numpy().astype(np.uint64)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return t.numpy().astype(np.uint64)
 

@@ -17,6 +17,7 @@ import argparse
 import ctypes as C
 import hashlib
 import json
+import os
 import subprocess
 import sys
 import tempfile
@@ -42,6 +43,15 @@ TRACES = {
     "c3_noise": (5000, 200, [(200, 20)] * 5, 0, 5, 0.35, 6, 0.2, 6, 600),
     "c4": (20000, 500, [(600, 20)] * 5, 0, 0, 0.0, 2026, 1e-9, 8, 600),
     "c5": (200000, 1000, [(6000, 30)] * 5, 0, 0, 0.0, 2027, 1e-9, 3, 600),
+}
+
+
+# Steady-state traces (late-run batches): the early
+# generations plus a sparse sample of the run up to `iterations`.
+STEADY = {
+    # name: (base trace, iterations, record_first, record_every)
+    "c4ss": ("c4", 5000, 8, 250),
+    "c5ss": ("c5", 1000, 50, 100),
 }
 
 
@@ -187,6 +197,40 @@ def fixture_trace(ref: oracle.Ref, name: str) -> None:
     print(f"trace {name}: {len(trace)} batches, {sum(sizes)} series", flush=True)
 
 
+def fixture_trace_steady(ref: oracle.Ref, name: str) -> None:
+    base, iterations, first, every = STEADY[name]
+    rows, cols, blocks, pattern, overlap, noise, seed, eps, _, pop = TRACES[base]
+    v = ref.generate(rows, cols, blocks, pattern, overlap, overlap, noise, seed)
+    m = ref.matrix(v)
+    sigma = int(ref.lib.ref_default_sigma(rows))
+    threads = os.cpu_count() or 8
+    with tempfile.TemporaryDirectory() as td:
+        path = Path(td) / "trace.bin"
+        n = ref.run_trace_sel(m, path, population=pop, iterations=iterations, rng_seed=1, eps=eps,
+                              sigma=0, threads=threads, record_first=first, record_every=every)
+        trace = oracle.read_trace_sel(path)
+    assert n == len(trace)
+    gens, lens, cols_all, counts, fits, sizes = [], [], [], [], [], []
+    for k, off, c, cnt in trace:
+        gens.append(k)
+        lens.append(np.diff(off).astype(np.uint16))
+        cols_all.append(c)
+        counts.append(cnt)
+        fits.append(ref.evaluate_population(m, off, c, sigma, eps, workers=threads))
+        sizes.append(len(cnt))
+    np.savez_compressed(
+        OUT / f"trace_{name}.npz",
+        spec=np.array(json.dumps(dict(rows=rows, cols=cols, blocks=blocks, pattern=pattern,
+                                      overlap=overlap, noise=noise, seed=seed))),
+        matrix_sha256=np.array(sha(v)), eps=np.array(eps), sigma=np.array(sigma),
+        generations=np.array(gens, dtype=np.uint32), iterations=np.array(iterations),
+        batch_sizes=np.array(sizes, dtype=np.uint32), lens=np.concatenate(lens),
+        cols=np.concatenate(cols_all), counts=np.concatenate(counts).astype(np.uint32),
+        fitness=np.concatenate(fits))
+    print(f"trace {name}: {len(trace)} batches (generations {gens[0]}..{gens[-1]}), "
+          f"{sum(sizes)} series", flush=True)
+
+
 # TopRankList::update sequences: whole populations as the
 # reference GA passes them to the list (elite clones + novel), and the random
 # stress streams with many fitness ties and column collisions.
@@ -280,6 +324,8 @@ def main() -> None:
             "top_rank": lambda: fixture_top_rank(ref)}
     for t in TRACES:
         jobs[t] = (lambda t=t: fixture_trace(ref, t))
+    for t in STEADY:
+        jobs[t] = (lambda t=t: fixture_trace_steady(ref, t))
     for name, job in jobs.items():
         if a.only and name != a.only:
             continue

@@ -89,3 +89,52 @@ def test_shard_range_partitions():
                 assert lo == lo_prev and hi >= lo
                 lo_prev = hi
             assert lo_prev == total
+
+
+def _bad_reduce_worker(port, q):
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    sys.path.insert(0, str(root))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_1801_03039_b200.distributed import RowShardedEvaluator
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        RowShardedEvaluator(np.zeros((4, 3)), reduce="kernal")
+        q.put("accepted")
+    except ValueError as e:
+        q.put(str(e))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_invalid_reduce_rejected_before_any_device_work():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_bad_reduce_worker, args=(_free_port(), q))
+    p.start()
+    out = q.get(timeout=120)
+    p.join(timeout=60)
+    assert "reduce must be" in out
+
+
+def test_bench_refuses_mismatched_world_size():
+    """A line whose rank count differs from --gpus would mislabel a scaling
+    run: bench.py refuses it (here WORLD_SIZE=2 but --gpus 3), and a
+    self-launched `--gpus 2` on a box without 2 GPUs refuses in every rank."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "3", "--steps", "3",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 2 and "refusing" in r.stderr
+    assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["CUDA_VISIBLE_DEVICES"] = ""
+    r = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "2", "--steps", "3",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode != 0 and "refusing" in r.stderr
+    assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
