@@ -34,6 +34,7 @@
 
 #include "../../include/ebic_b200.h"
 #include "kernels.cuh"
+#include "kernels_v2.cuh"
 
 using namespace ebic_b200;
 
@@ -94,7 +95,8 @@ int env_int(const char* name, int dflt) {
 // context is created so the per-generation launch path makes no getenv calls.
 struct Knobs {
     int force_direct, rpg, rpl, stages, ncw, slice, layout_f64, no_collapse, sched_static,
-        max_parts, reduce_tree, grid, phase_timing, spg, host_copy, xshard, graph, debug_mode;
+        max_parts, reduce_tree, grid, phase_timing, spg, host_copy, xshard, graph, debug_mode, kernel,
+        gap, compact, v2_ncw;
     static Knobs from_env() {
         Knobs k;
         k.force_direct = env_int("EBIC_FORCE_DIRECT", 0);
@@ -115,6 +117,14 @@ struct Knobs {
         k.xshard = env_int("EBIC_XSHARD", 1);  // in-kernel cross-shard reduction
         k.graph = env_int("EBIC_GRAPH", 1);    // count launches through a cached one-node graph
         k.debug_mode = env_int("EBIC_DEBUG_MODE", 0);  // measurement only: wrong results
+        // rank layouts: 2 = K1v2 (column-compacted staging, default), 1 = the
+        // v1 TMA-tile kernel; the v1 tile knobs select v1 as well
+        k.kernel = env_int("EBIC_KERNEL", 2);
+        if (k.slice || k.rpg || k.rpl || k.spg || k.ncw) k.kernel = 1;
+        k.gap = env_int("EBIC_GAP", 0);  // K1v2: unreferenced gap columns staged with their runs
+        // K1v2 staging: -1 auto (referenced columns only for long launches), 0 whole tiles, 1 compact
+        k.compact = env_int("EBIC_COMPACT", -1);
+        k.v2_ncw = env_int("EBIC_V2_NCW", 24);
         return k;
     }
 };
@@ -153,6 +163,7 @@ constexpr size_t kMaxLenPerLaunch = 8192;
 
 // Kernel configuration of the TMA count kernel for one shard.
 struct CountConfig {
+    int v2 = 0;         // 1: K1v2 (kernels_v2.cuh) over the tile-major rank matrix
     int layout = 0;     // 0 = fp64 tile, 1 = rank (1 plane), 2 = rank (2 planes)
     int rpg = 0;        // rows per tile (0 = direct kernel)
     int rpl = 1;        // rows per lane
@@ -556,6 +567,28 @@ CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int
     const int want_stages = kn.stages;
     const int want_ncw = kn.ncw;
     const size_t budget = (size_t)s.max_smem;
+    if (rank_planes && kn.kernel == 2) {
+        // K1v2: the whole opt-in window; one stage must fit even if the
+        // launch referenced min(C, L) columns (the ring depth follows the
+        // actual U at run time)
+        const V2Layout v = v2_layout((uint32_t)P, (uint32_t)L, (uint32_t)n_cols);
+        const size_t window = budget - 1024 - 128;  // static shared bytes + alignment
+        const size_t worst = std::min(n_cols, L) * 128;
+        if (v.area < window && window - v.area >= std::max<size_t>(worst, v2_scratch_bytes((uint32_t)P, (uint32_t)L))) {
+            CountConfig c;
+            c.v2 = 1;
+            c.layout = rank_planes;
+            c.slice = 128;
+            c.rpg = rank_planes == 2 ? 32 : 64;
+            c.rpl = rank_planes == 2 ? 4 : 8;
+            c.ncw = 24;
+            c.spg = 2;
+            c.stages = kn.stages;  // 0: as many as fit (<= 4)
+            // a lane's 16-bit partial counts grow by <= 8 rows per tile it walks
+            const size_t tiles = (s.rows + c.rpg - 1) / c.rpg;
+            if ((tiles / std::max(1, std::min<int>((int)tiles, s.sm_count)) + 2) * 8 <= 0xffff) return c;
+        }
+    }
     if (rank_planes) {
         const int want_slice = kn.slice;
         for (int min_stages : {3, 2}) {
@@ -835,8 +868,12 @@ RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
 const CUtensorMap& rank_tensor_map(RankLayout& rl, const Shard& s, size_t n_cols, const CountConfig& cfg) {
     if (!rl.tmap_ok || rl.tmap_slice != cfg.slice) {
         rl.tmap_slice = cfg.slice;
-        cuuint64_t dims[2] = {(cuuint64_t)(s.ld * rl.planes), (cuuint64_t)n_cols};
-        cuuint64_t strides[1] = {(cuuint64_t)(s.ld * rl.planes * sizeof(uint16_t))};
+        // tile-major rank matrix seen as [blocks * n_cols][64 u16] (one row
+        // per 128-byte block of one column); a box is one slice of box_cols
+        // consecutive columns of a block
+        const size_t rows_per_block = rl.planes == 2 ? 32 : 64;
+        cuuint64_t dims[2] = {64, (cuuint64_t)(s.ld / rows_per_block * n_cols)};
+        cuuint64_t strides[1] = {128};
         cuuint32_t box[2] = {(cuuint32_t)(cfg.slice / 2), cfg.box_cols};  // one column slice
         cuuint32_t estr[2] = {1, 1};
         CUresult r = tensor_map_encoder()(&rl.tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, rl.d, dims,
@@ -939,6 +976,67 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         s.memo_P = P, s.memo_L = L, s.memo_planes = planes;
     }
     const CountConfig c = s.memo_cfg;
+    if (c.v2) {
+        p.ranks = reinterpret_cast<const unsigned char*>(rl->d);
+        p.stages = (uint32_t)c.stages;
+        p.n_tiles = (uint32_t)((s.rows + c.rpg - 1) / c.rpg);
+        const size_t smem = (size_t)s.max_smem - 1024;  // leaves room for the static shared bytes
+        p.smem_window = (uint32_t)(smem - 128);
+        int grid = std::min<int>((int)p.n_tiles, s.sm_count);
+        if (s.knobs.grid > 0) grid = std::min<int>(s.knobs.grid, (int)p.n_tiles);
+        // per-CTA counts in 16-bit halves while a CTA's rows fit
+        p.gap = (uint32_t)std::min(std::max(s.knobs.gap, 0), 2);
+        // Whole tiles (one contiguous copy each, issued at once) for short
+        // launches; the referenced columns only once a CTA walks enough tiles
+        // to amortise building the column set first, or when two whole-tile
+        // stages do not fit.
+        const V2Layout vl = v2_layout((uint32_t)P, (uint32_t)L, (uint32_t)ctx.n_cols);
+        const size_t area = p.smem_window - vl.area;
+        const size_t block = ctx.n_cols * 128;
+        uint32_t full_stages = (uint32_t)std::min<size_t>(kV2MaxStages, area / block);
+        if (c.stages > 0) full_stages = std::min<uint32_t>(full_stages, (uint32_t)c.stages);
+        const bool long_launch = p.n_tiles >= 6u * (uint32_t)grid;
+        bool compact = long_launch || full_stages < 2;
+        if (s.knobs.compact == 0 && full_stages >= 1) compact = false;
+        if (s.knobs.compact == 1) compact = true;
+        p.compact = compact ? 1u : 0u;
+        if (!compact) p.stages = full_stages;
+        s.last_grid = grid;
+        s.last_cfg = c;
+        s.last_collapsed = rl->collapsed;
+        ensure_partial(s, P, grid, p.reduce_striped != 0);
+        p.partial = s.d_partial;
+        if (rl->collapsed) {
+            p.rank_k = 0x80008000u;
+            p.row_excl = rl->d_row_excl;
+            p.excl_rows = rl->d_excl_rows;
+            p.excl_vals = rl->d_excl_vals;
+            p.n_excl = rl->n_excl;
+        } else {
+            p.rank_k = 0x7fff7fffu;
+        }
+        // consumer warps (EBIC_V2_NCW: 20, 24 default, 28)
+        const int ncw = s.knobs.v2_ncw == 20 ? 20 : s.knobs.v2_ncw == 28 ? 28 : 24;
+        const void* fn;
+        if (c.layout == 2)
+            fn = ncw == 20 ? reinterpret_cast<const void*>(count_v2_kernel<2, 20>)
+               : ncw == 28 ? reinterpret_cast<const void*>(count_v2_kernel<2, 28>)
+                           : reinterpret_cast<const void*>(count_v2_kernel<2, 24>);
+        else
+            fn = ncw == 20 ? reinterpret_cast<const void*>(count_v2_kernel<1, 20>)
+               : ncw == 28 ? reinterpret_cast<const void*>(count_v2_kernel<1, 28>)
+                           : reinterpret_cast<const void*>(count_v2_kernel<1, 24>);
+        static std::atomic<int> v2_smem_set[2][3][64] = {};
+        std::atomic<int>& flag = v2_smem_set[c.layout - 1][ncw == 20 ? 0 : ncw == 28 ? 2 : 1][s.device & 63];
+        if (flag.load(std::memory_order_acquire) < (int)smem) {
+            CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            flag.store((int)smem, std::memory_order_release);
+        }
+        void* args[1] = {const_cast<CountParams*>(&p)};
+        launch_kernel(&s, fn, grid, (ncw + kV2Producers) * 32, smem, st, args);
+        CK(cudaGetLastError());
+        return;
+    }
     if (c.rpg) {
         p.box_cols = c.box_cols;
         p.n_boxes = c.n_boxes;

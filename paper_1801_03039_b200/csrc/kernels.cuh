@@ -55,16 +55,18 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    // try_wait with a suspend-time hint: a waiting warp sleeps until the
+    // phase completes (or the hint expires) instead of re-issuing the probe
     asm volatile(
         "{\n"
         ".reg .pred P1;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
         "@P1 bra DONE_%=;\n"
         "bra WAIT_%=;\n"
         "DONE_%=:\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)
         : "memory");
 }
 
@@ -192,8 +194,14 @@ struct CountParams {
     unsigned long long* __restrict__ phase_ns;  // optional [grid][8] %globaltimer stamps
     // Measurement only (EBIC_DEBUG_MODE; results are wrong): 1 = consumers
     // skip the walk (pure TMA streaming time), 2 = the producer skips the
-    // loads (pure walk time over stale stages).
+    // loads (pure walk time over stale stages), 3 (K1v2) = no ring at all:
+    // consumers walk stage 0 item after item (intrinsic walk rate).
     uint32_t debug_mode;
+    // K1v2 (kernels_v2.cuh): tile-major rank matrix, usable dynamic shared bytes
+    const unsigned char* __restrict__ ranks;
+    uint32_t smem_window;
+    uint32_t gap;         // K1v2: stage gaps of <= gap unreferenced columns (0-2)
+    uint32_t compact;     // K1v2: stage the referenced columns (1) or whole tiles (0)
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -647,6 +655,7 @@ struct F64Walker {
     static constexpr int kLaneBytes = RPL * 8;
     static constexpr int kColBytes = RPG * 8;      // one column of a staged tile
     static constexpr int kDim0PerTile = RPG;       // TMA dim-0 extent of a tile (fp64 elements)
+    static constexpr bool kTileMajor = false;      // column-major fp64 matrix
     using Mask = uint32_t;
     // excl: bit k set = the lane's row k is excluded (fixed up separately).
     __device__ __forceinline__ static Mask valid(uint32_t row0, uint32_t n_rows, uint32_t excl,
@@ -787,6 +796,10 @@ struct RankWalker {
     static constexpr int kColBytes = SLICE;
     static constexpr int kShift = SLICE == 128 ? 7 : 6;
     static constexpr int kDim0PerTile = kRowsPerTile * PLANES;  // u16 elements
+    // The rank matrix is tile-major (rank_build_kernel): 128-byte blocks of
+    // one column's rows, [block][column][64 u16]; a 64-byte slice is half a block.
+    static constexpr bool kTileMajor = true;
+    static constexpr int kSlicesPerBlock = 128 / SLICE;
     static constexpr int kWords = kRowsPerLane / 2;           // ok words per lane
     static constexpr int kSeriesPerGroup = SPG;               // independent walks per group
     static constexpr int kFieldBits = 32 / SPG;               // packed per-series counts
@@ -1088,10 +1101,19 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                 } else {
                     mbar_arrive_expect_tx(&full_bar[st], p.stage_bytes);
                     unsigned char* dst = stage_base + size_t(st) * p.stage_bytes;
+                    // fp64: column-major [cols][ld]; ranks: tile-major, the tensor
+                    // viewed as [blocks * cols][64 u16] (one row per 128-byte block)
+                    int c0, c1;
+                    if constexpr (Walker::kTileMajor) {
+                        c0 = static_cast<int>((tile % Walker::kSlicesPerBlock) * Walker::kDim0PerTile);
+                        c1 = static_cast<int>((tile / Walker::kSlicesPerBlock) * p.n_cols);
+                    } else {
+                        c0 = static_cast<int>(tile * Walker::kDim0PerTile);
+                        c1 = 0;
+                    }
                     for (uint32_t b = 0; b < p.n_boxes; ++b)
                         tma_load_2d(dst + size_t(b) * p.box_cols * Walker::kColBytes, &tmap,
-                                    &full_bar[st], static_cast<int>(tile * Walker::kDim0PerTile),
-                                    static_cast<int>(b * p.box_cols));
+                                    &full_bar[st], c0, c1 + static_cast<int>(b * p.box_cols));
                 }
                 if (++st == p.stages) st = 0, phase ^= 1u;
             }
@@ -1283,9 +1305,16 @@ __global__ void __launch_bounds__(256)
     uint32_t* wsum = rk + Kp;
     const uint32_t r = blockIdx.x;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const size_t cs = PLANES == 2 ? size_t(ld) * 2 : size_t(ld);  // u16 per column
+    // Tile-major: 128-byte blocks [block][column][64 u16], a block holding 64
+    // rows (one plane) or 32 rows as lo[4] hi[4] per 4 rows (two planes), so
+    // a row tile is one contiguous n_cols * 128-byte range and any column
+    // subset of it is a list of 128-byte slices.
+    constexpr uint32_t kRowsPerBlock = PLANES == 2 ? 32 : 64;
+    const size_t block_u16 = size_t(n_cols) * 64;
     auto at = [&](uint32_t c, uint32_t plane) -> size_t {
-        return PLANES == 2 ? c * cs + (r >> 2) * 8 + plane * 4 + (r & 3) : c * cs + r;
+        const size_t b = size_t(r / kRowsPerBlock) * block_u16 + size_t(c) * 64;
+        const uint32_t q = r % kRowsPerBlock;
+        return PLANES == 2 ? b + (q >> 2) * 8 + plane * 4 + (q & 3) : b + q;
     };
     if (r >= n_rows) {  // padding rows: fail every test
         for (uint32_t c = tid; c < n_cols; c += nt) {

@@ -1,0 +1,698 @@
+// kernels_v2.cuh -- K1v2: the count kernel over the tile-major rank matrix
+// with column-compacted staging.
+//
+// Same contract as count_tma_kernel (per-series match counts of one
+// population over one row shard + the fused Eq. 1 epilogue,
+// /root/reference/proj/include/ebic/fitness.hpp:71-143); differences:
+//
+//  * Staging.  A launch references U of the matrix's C columns (GA batches:
+//    U ~ 0.6 C at 200,000 x 1000, ~0.9 C at 20,000 x 500).  The rank matrix
+//    is tile-major (rank_build_kernel: [block][column][128 B]), so the U
+//    referenced slices of a row tile are the launch's runs of consecutive
+//    referenced columns, each one contiguous range: the producer warps copy
+//    one run per cp.async.bulk into consecutive slots of the stage.  HBM
+//    moves rows x U x 2 B instead of rows x C x 2 B, and a stage of 64-row
+//    tiles (128-byte slices: one whole bank row per lane group, no bank
+//    conflicts) fits twice or more in shared memory where the full tile
+//    fitted only with 32-row tiles.  The ring depth follows U at run time.
+//  * Walk.  Slots are length-sorted; a chunk (8 consecutive slots, 4 lane
+//    groups x 2 series) of one length <= 12 is described by one word
+//    (length, first list entry), so the walk loads no per-slot metadata:
+//    slot lists are consecutive with stride pad4(length).  Chunks are
+//    assigned to warps statically (longest first, rotated every tile), and
+//    every lane adds its own partial counts into a private word of the chunk
+//    (16-bit halves for the chunk's two series per group): no dispenser, no
+//    per-chunk shuffles, no contended atomics; the words are summed once.
+//
+// Producer warps build the column bitmap, slots and runs from the CBF while
+// the consumer warps sort the population; both meet at `cols_ready`.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace ebic_b200 {
+
+constexpr int kV2Producers = 4;     // producer warps (bulk-copy issue is per lane)
+constexpr int kV2MaxCols = 2048;    // bitmap of 64 words
+constexpr int kV2Chunk = 8;         // slots per warp iteration (4 groups x 2 series)
+constexpr int kV2MaxStages = 4;
+
+// Byte offsets of the persistent work list inside the dynamic window.
+struct V2Layout {
+    uint32_t bars;      // full[kMaxStages], empty[kMaxStages], prol, cols  (u64)
+    uint32_t misc;      // u32[16]: U, n_runs, stages, ...
+    uint32_t next;      // u32[kMaxStages] chunk dispensers
+    uint32_t sl, slen, sstart, cnt, cdesc;
+    uint32_t pcols;     // u32[L + 3P], 16-byte aligned lists
+    uint32_t bm, bases; // u32[64] each
+    uint32_t ucols;     // u16[n_cols] slot -> column
+    uint32_t runs, run_slot;  // u32[max_runs] each
+    uint32_t acc;       // u32[n_chunks][32] per-lane partial counts (owned schedule)
+    uint32_t area;      // first byte of the stage area (128-aligned)
+};
+
+__host__ __device__ inline uint32_t v2_max_runs(uint32_t n_cols) { return (n_cols + 1) / 2 + 1; }
+
+__host__ __device__ inline V2Layout v2_layout(uint32_t P, uint32_t L, uint32_t n_cols) {
+    auto up16 = [](uint32_t x) { return (x + 15u) & ~15u; };
+    V2Layout v;
+    uint32_t at = 0;
+    v.bars = at;     at += (2 * kMaxStages + 2) * 8;
+    v.misc = at;     at += 16 * 4;
+    v.next = at;     at += kMaxStages * 4;
+    at = up16(at);
+    v.sl = at;       at = up16(at + 4 * P);
+    v.slen = at;     at = up16(at + 4 * P);
+    v.sstart = at;   at = up16(at + 4 * P);
+    v.cnt = at;      at = up16(at + 4 * (P + 2));
+    v.cdesc = at;    at = up16(at + 4 * ((P + kV2Chunk - 1) / kV2Chunk));
+    v.pcols = at;    at = up16(at + 4 * (L + 3 * P));
+    v.bm = at;       at += 64 * 4;
+    v.bases = at;    at += 64 * 4;
+    v.ucols = at;    at = up16(at + 2 * n_cols);
+    v.runs = at;     at = up16(at + 4 * v2_max_runs(n_cols));
+    v.run_slot = at; at = up16(at + 4 * v2_max_runs(n_cols));
+    v.acc = at;      at = up16(at + 4 * 32 * ((P + kV2Chunk - 1) / kV2Chunk));
+    v.area = (at + 127u) & ~127u;
+    return v;
+}
+
+// Prologue scratch (dead once the work list is built), at the END of the
+// stage area: rel u32[P+1], raw u16[L+16], wh u32[ceil(P/32)*64], hist,
+// hpad u32[64], wsum u32[32] -- the v1 builder's scratch.
+__host__ __device__ inline uint32_t v2_scratch_bytes(uint32_t P, uint32_t L) {
+    return static_cast<uint32_t>(count_scratch_bytes(P, L));
+}
+
+__device__ __forceinline__ uint32_t v2_slot_of(const uint32_t* bm, const uint32_t* bases, uint32_t c) {
+    return bases[c >> 5] + __popc(bm[c >> 5] & ((1u << (c & 31)) - 1u));
+}
+
+// Producer warps: column bitmap, slots, runs (from the CBF).  All
+// kV2Producers warps load and mark; warp 0 then derives bases, ucols, runs.
+__device__ __forceinline__ void v2_build_columns(const CountParams& p, unsigned char* smem, const V2Layout& v,
+                                                 int pw, int lane) {
+    uint32_t* bm = reinterpret_cast<uint32_t*>(smem + v.bm);
+    const int ptid = pw * 32 + lane;
+    constexpr int nthr = kV2Producers * 32;
+    for (int w = ptid; w < 64; w += nthr) bm[w] = 0;
+    named_bar_sync(2, nthr);
+    const uint32_t L = p.total_len;
+    const uint16_t* src = p.cols + p.cols_base;
+    const uint32_t shift = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) & 15u) >> 1);
+    const uint4* vsrc = reinterpret_cast<const uint4*>(src - shift);
+    const uint32_t n_vec = (shift + L + 7u) >> 3;
+    constexpr int kPer = 4;
+    for (uint32_t i0 = ptid; i0 < n_vec; i0 += kPer * nthr) {
+        uint4 x[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const uint32_t i = i0 + k * nthr;
+            if (i < n_vec) x[k] = __ldcg(vsrc + i);
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const uint32_t i = i0 + k * nthr;
+            if (i >= n_vec) continue;
+            const uint32_t w4[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                const uint32_t pos = i * 8 + h;  // position from the aligned word
+                if (pos < shift || pos >= shift + L) continue;
+                const uint32_t c = (w4[h >> 1] >> (16 * (h & 1))) & 0xffffu;
+                atomicOr(&bm[c >> 5], 1u << (c & 31));
+            }
+        }
+    }
+    named_bar_sync(2, nthr);
+    if (pw != 0) return;
+    uint32_t* bases = reinterpret_cast<uint32_t*>(smem + v.bases);
+    uint16_t* ucols = reinterpret_cast<uint16_t*>(smem + v.ucols);
+    uint32_t* runs = reinterpret_cast<uint32_t*>(smem + v.runs);
+    uint32_t* run_slot = reinterpret_cast<uint32_t*>(smem + v.run_slot);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + v.misc);
+    // word w = lane (low half) and lane + 32 (high half); column order =
+    // word order 0..63.  Gaps of <= p.gap unreferenced columns between two
+    // referenced ones are staged too (fewer, longer copies); the staged set
+    // replaces the bitmap, and slots follow it.
+    uint32_t x0 = bm[lane], x1 = bm[lane + 32];
+    if (p.gap) {
+        const uint32_t a0 = __shfl_up_sync(0xffffffffu, x0, 1), a1 = __shfl_up_sync(0xffffffffu, x1, 1);
+        const uint32_t n0 = __shfl_down_sync(0xffffffffu, x0, 1), n1 = __shfl_down_sync(0xffffffffu, x1, 1);
+        const uint32_t w31 = __shfl_sync(0xffffffffu, x0, 31), w32 = __shfl_sync(0xffffffffu, x1, 0);
+        const uint32_t pv0 = lane == 0 ? 0u : a0, pv1 = lane == 0 ? w31 : a1;
+        const uint32_t nx0 = lane == 31 ? w32 : n0, nx1 = lane == 31 ? 0u : n1;
+        auto fill = [&](uint32_t x, uint32_t prev, uint32_t next) {
+            const uint32_t m1 = (x << 1) | (prev >> 31), m2 = (x << 2) | (prev >> 30);
+            const uint32_t q1 = (x >> 1) | (next << 31), q2 = (x >> 2) | (next << 30);
+            uint32_t f = m1 & q1;                        // gap of one column
+            if (p.gap >= 2) f |= (m1 & q2) | (m2 & q1);  // gap of two
+            return x | f;
+        };
+        const uint32_t c0 = fill(x0, pv0, nx0), c1 = fill(x1, pv1, nx1);
+        __syncwarp();
+        x0 = c0;
+        x1 = c1;
+        bm[lane] = x0;
+        bm[lane + 32] = x1;
+        __syncwarp();
+    }
+    auto excl_scan = [&](uint32_t a, uint32_t& total) {
+        uint32_t incl = a;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        total = __shfl_sync(0xffffffffu, incl, 31);
+        return incl - a;
+    };
+    uint32_t t0, t1;
+    const uint32_t b0 = excl_scan(__popc(x0), t0);
+    const uint32_t b1 = t0 + excl_scan(__popc(x1), t1);
+    bases[lane] = b0;
+    bases[lane + 32] = b1;
+    const uint32_t U = t0 + t1;
+    {
+        uint32_t x = x0, at = b0;
+        while (x) {
+            const int j = __ffs(x) - 1;
+            ucols[at++] = static_cast<uint16_t>(lane * 32 + j);
+            x &= x - 1;
+        }
+        x = x1;
+        at = b1;
+        while (x) {
+            const int j = __ffs(x) - 1;
+            ucols[at++] = static_cast<uint16_t>((lane + 32) * 32 + j);
+            x &= x - 1;
+        }
+    }
+    // runs: start bit = set with the previous column clear; end bit = set
+    // with the next column clear (bits of the neighbouring words via shuffles)
+    const uint32_t prev_top0 = __shfl_up_sync(0xffffffffu, x0 >> 31, 1);
+    const uint32_t x0_last = __shfl_sync(0xffffffffu, x0, 31);
+    const uint32_t prev_top1_raw = __shfl_up_sync(0xffffffffu, x1 >> 31, 1);
+    const uint32_t pt0 = lane == 0 ? 0u : prev_top0;
+    const uint32_t pt1 = lane == 0 ? (x0_last >> 31) : prev_top1_raw;
+    const uint32_t next_bot0_raw = __shfl_down_sync(0xffffffffu, x0 & 1u, 1);
+    const uint32_t x1_first = __shfl_sync(0xffffffffu, x1, 0);
+    const uint32_t next_bot1_raw = __shfl_down_sync(0xffffffffu, x1 & 1u, 1);
+    const uint32_t nb0 = lane == 31 ? (x1_first & 1u) : next_bot0_raw;
+    const uint32_t nb1 = lane == 31 ? 0u : next_bot1_raw;
+    const uint32_t s0 = x0 & ~((x0 << 1) | pt0), s1 = x1 & ~((x1 << 1) | pt1);
+    const uint32_t e0 = x0 & ~((x0 >> 1) | (nb0 << 31)), e1 = x1 & ~((x1 >> 1) | (nb1 << 31));
+    uint32_t ts0, ts1, te0, te1;
+    const uint32_t rs0 = excl_scan(__popc(s0), ts0);
+    const uint32_t rs1 = ts0 + excl_scan(__popc(s1), ts1);
+    const uint32_t re0 = excl_scan(__popc(e0), te0);
+    const uint32_t re1 = te0 + excl_scan(__popc(e1), te1);
+    const uint32_t n_runs = ts0 + ts1;
+    // starts into runs[] (column), ends into run_slot[] temporarily
+    auto put = [&](uint32_t x, uint32_t at, uint32_t word, uint32_t* out) {
+        while (x) {
+            const int j = __ffs(x) - 1;
+            out[at++] = word * 32 + j;
+            x &= x - 1;
+        }
+    };
+    put(s0, rs0, lane, runs);
+    put(s1, rs1, lane + 32, runs);
+    put(e0, re0, lane, run_slot);
+    put(e1, re1, lane + 32, run_slot);
+    __syncwarp();
+    for (uint32_t r = lane; r < n_runs; r += 32) {
+        const uint32_t c0 = runs[r], c1 = run_slot[r];
+        runs[r] = (c0 << 16) | (c1 - c0 + 1);
+        run_slot[r] = v2_slot_of(bm, bases, c0);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        misc[0] = U;
+        misc[1] = n_runs;
+    }
+    __syncwarp();
+}
+
+// Consumer-side work list (NCW warps): the v1 counting sort by length
+// (build_work_list phases A-C), then lists of slot byte offsets (slot x 128)
+// once the producer's column slots are ready, then chunk descriptors.
+template <int CHUNK>
+__device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigned char* smem, const V2Layout& v,
+                                                   const WorkList& w, uint64_t* cols_ready, int tid, int nthreads,
+                                                   int bar_id) {
+    const uint32_t P = p.n_series, L = p.total_len;
+    const uint32_t nblk = (P + 31) / 32;
+    const int lane = tid & 31, nw = nthreads >> 5;
+    const uint64_t base = p.cols_base;
+    const uint16_t* src = p.cols + base;
+    const uint32_t shift = static_cast<uint32_t>((reinterpret_cast<uintptr_t>(src) & 15u) >> 1);
+    const uint4* vsrc = reinterpret_cast<const uint4*>(src - shift);
+    const uint32_t n_vec = (shift + L + 7u) >> 3;
+    constexpr int kPer = 4;
+    for (uint32_t s0 = tid; s0 <= P || s0 < n_vec; s0 += kPer * nthreads) {
+        uint64_t o[kPer];
+        uint4 x[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const uint32_t i = s0 + k * nthreads;
+            if (i <= P) o[k] = __ldcg(p.offsets + i);
+            if (i < n_vec) x[k] = __ldcg(vsrc + i);
+        }
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const uint32_t i = s0 + k * nthreads;
+            if (i <= P) w.rel[i] = static_cast<uint32_t>(o[k] - base) + shift;
+            if (i < n_vec) reinterpret_cast<uint4*>(w.raw)[i] = x[k];
+        }
+    }
+    for (uint32_t i = tid; i < nblk * kLenBuckets; i += nthreads) w.wh[i] = 0;
+    for (int b = tid; b < kLenBuckets; b += nthreads) w.hist[b] = 0;
+    named_bar_sync(bar_id, nthreads);  // 1
+
+    auto bucket_of = [&](uint32_t s, uint32_t& len) -> uint32_t {
+        len = s < P ? w.rel[s + 1] - w.rel[s] : 0u;
+        return s < P ? (len < kLenBuckets ? len : kLenBuckets - 1) : 0xffffu;
+    };
+    for (uint32_t blk = tid >> 5; blk < nblk; blk += nw) {
+        uint32_t len;
+        const uint32_t bkt = bucket_of(blk * 32 + lane, len);
+        const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
+        if (bkt != 0xffffu && lane == __ffs(peers) - 1) {
+            w.wh[blk * kLenBuckets + bkt] = __popc(peers);
+            atomicAdd(&w.hist[bkt], static_cast<uint32_t>(__popc(peers)));
+        }
+    }
+    named_bar_sync(bar_id, nthreads);  // 2
+
+    if (tid < 32) {
+        for (int k = 0; k < 2; ++k) {
+            const int b = tid + 32 * k;
+            w.hpad[b] = b < kLenBuckets - 1 ? w.hist[b] * pad4(b) : 0u;
+        }
+        __syncwarp();
+        warp_scan64(w.hist, w.hpad, tid);
+    } else if (tid < 32 + kLenBuckets) {
+        const int b = tid - 32;
+        uint32_t run = 0;
+        for (uint32_t blk = 0; blk < nblk; ++blk) {
+            const uint32_t t = w.wh[blk * kLenBuckets + b];
+            w.wh[blk * kLenBuckets + b] = run;
+            run += t;
+        }
+    }
+    if (cols_ready) mbar_wait(cols_ready, 0);  // producer: bitmap + slot bases (compact staging)
+    named_bar_sync(bar_id, nthreads);  // 3
+
+    const uint32_t* bm = reinterpret_cast<const uint32_t*>(smem + v.bm);
+    const uint32_t* bases = reinterpret_cast<const uint32_t*>(smem + v.bases);
+    const bool compact = cols_ready != nullptr;
+    auto slot_of = [&](uint32_t c) -> uint32_t { return compact ? v2_slot_of(bm, bases, c) : c; };
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t blk = tid >> 5; blk < nblk; blk += nw) {
+        uint32_t len;
+        const uint32_t s = blk * 32 + lane;
+        const uint32_t bkt = bucket_of(s, len);
+        const uint32_t peers = __match_any_sync(0xffffffffu, bkt);
+        if (bkt == 0xffffu) continue;
+        const uint32_t r = w.wh[blk * kLenBuckets + bkt] + __popc(peers & lt);
+        const uint32_t g = w.hist[bkt] + r;
+        w.sl[g] = s;
+        w.slen[g] = len;
+        if (bkt < kLenBuckets - 1) {
+            const uint32_t st = w.hpad[bkt] + r * pad4(len);
+            w.sstart[g] = st;
+            const uint16_t* from = w.raw + w.rel[s];
+            for (uint32_t i = 0; i < pad4(len); ++i)
+                w.pcols[st + i] = i < len ? slot_of(from[i]) * 128u : 0u;
+        }
+    }
+    for (uint32_t i = tid; i < P + 2; i += nthreads) w.cnt[i] = 0;
+    {
+        uint32_t* acc = reinterpret_cast<uint32_t*>(smem + v.acc);
+        const uint32_t n_acc = 32u * ((P + CHUNK - 1) / CHUNK);
+        for (uint32_t i = tid; i < n_acc; i += nthreads) acc[i] = 0;
+    }
+    named_bar_sync(bar_id, nthreads);  // 4
+
+    const uint32_t ovf = w.hist[kLenBuckets - 1];
+    if (ovf < P) {
+        if (tid == 0) {
+            uint32_t run = w.hpad[kLenBuckets - 1];
+            for (uint32_t g = ovf; g < P; ++g) {
+                w.sstart[g] = run;
+                run += pad4(w.slen[g]);
+            }
+        }
+        named_bar_sync(bar_id, nthreads);
+        for (uint32_t g = ovf + tid; g < P; g += nthreads) {
+            const uint32_t len = w.slen[g], st = w.sstart[g];
+            const uint16_t* from = w.raw + w.rel[w.sl[g]];
+            for (uint32_t i = 0; i < pad4(len); ++i)
+                w.pcols[st + i] = i < len ? slot_of(from[i]) * 128u : 0u;
+        }
+    }
+    // chunk descriptors: (first list entry << 8) | length for a full chunk of
+    // one length in [2, 12] (its lists are consecutive, stride pad4(length)),
+    // else 0 (per-slot path)
+    uint32_t* cdesc = reinterpret_cast<uint32_t*>(smem + v.cdesc);
+    const uint32_t n_chunks = (P + CHUNK - 1) / CHUNK;
+    for (uint32_t ch = tid; ch < n_chunks; ch += nthreads) {
+        const uint32_t first = ch * CHUNK;
+        const uint32_t l0 = w.slen[first];
+        const bool uni = first + CHUNK <= P && w.slen[first + CHUNK - 1] == l0 && l0 >= 2 && l0 <= 12;
+        cdesc[ch] = uni ? ((w.sstart[first] << 8) | l0) : 0u;
+    }
+    named_bar_sync(bar_id, nthreads);  // 5
+}
+
+// Two series of exactly L columns per lane group; lists at pc and pc + stride.
+template <class W, int L>
+__device__ __forceinline__ uint32_t v2_count2(uint32_t base, const uint32_t* pc, uint32_t stride,
+                                              const typename W::Mask& vm) {
+    constexpr int kWords = W::kWords;
+    const uint32_t* pa = pc;
+    const uint32_t* pb = pc + stride;
+    uint4 wa = *reinterpret_cast<const uint4*>(pa);
+    uint4 wb = *reinterpret_cast<const uint4*>(pb);
+    uint32_t oka[kWords], okb[kWords];
+#pragma unroll
+    for (int k = 0; k < kWords; ++k) oka[k] = okb[k] = 0xffffffffu;
+    uint4 preva = W::ld(base, wa.x), prevb = W::ld(base, wb.x);
+#pragma unroll
+    for (int i = 1; i < L; ++i) {
+        if ((i & 3) == 0) {
+            wa = *reinterpret_cast<const uint4*>(pa + i);
+            wb = *reinterpret_cast<const uint4*>(pb + i);
+        }
+        const uint32_t oa = (i & 3) == 0 ? wa.x : (i & 3) == 1 ? wa.y : (i & 3) == 2 ? wa.z : wa.w;
+        const uint32_t ob = (i & 3) == 0 ? wb.x : (i & 3) == 1 ? wb.y : (i & 3) == 2 ? wb.z : wb.w;
+        const uint4 cura = W::ld(base, oa);
+        const uint4 curb = W::ld(base, ob);
+        W::step(oka, preva, cura, vm.k);
+        W::step(okb, prevb, curb, vm.k);
+        preva = cura;
+        prevb = curb;
+    }
+    return W::tally(oka, vm) | (W::tally(okb, vm) << 16);
+}
+
+template <class W>
+__device__ __forceinline__ uint32_t v2_count_uniform(uint32_t L, uint32_t base, const uint32_t* pc, uint32_t stride,
+                                                     const typename W::Mask& vm) {
+    switch (L) {
+        case 2: return v2_count2<W, 2>(base, pc, stride, vm);
+        case 3: return v2_count2<W, 3>(base, pc, stride, vm);
+        case 4: return v2_count2<W, 4>(base, pc, stride, vm);
+        case 5: return v2_count2<W, 5>(base, pc, stride, vm);
+        case 6: return v2_count2<W, 6>(base, pc, stride, vm);
+        case 7: return v2_count2<W, 7>(base, pc, stride, vm);
+        case 8: return v2_count2<W, 8>(base, pc, stride, vm);
+        case 9: return v2_count2<W, 9>(base, pc, stride, vm);
+        case 10: return v2_count2<W, 10>(base, pc, stride, vm);
+        case 11: return v2_count2<W, 11>(base, pc, stride, vm);
+        default: return v2_count2<W, 12>(base, pc, stride, vm);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1v2.  PLANES: 1 (64-row tiles) or 2 (32-row tiles); 128-byte slices.
+// Grid: persistent, <= SMs; block: (NCW + kV2Producers) warps.
+// p.compact: stage the launch's referenced columns (runs); else whole tiles,
+// one contiguous bulk copy each (short launches: no wait for the column set).
+// ---------------------------------------------------------------------------
+template <int PLANES, int NCW>
+__global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
+    count_v2_kernel(const CountParams p) {
+    using W = RankWalker<PLANES, 128, 2>;
+    constexpr int RPG = W::kRowsPerTile;  // 64 or 32
+    constexpr int RPL = W::kRowsPerLane;
+    constexpr int GL = RPG / RPL;         // 8 lanes per group
+    constexpr int GW = 32 / GL;           // 4 groups per warp
+    constexpr int SPG = 2;
+    constexpr uint32_t CHUNK = GW * SPG;
+    static_assert(CHUNK == kV2Chunk, "chunk geometry");
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    const uint32_t P = p.n_series, Lt = p.total_len;
+    const V2Layout v = v2_layout(P, Lt, p.n_cols);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + v.bars);
+    uint64_t* empty_bar = full_bar + kMaxStages;
+    uint64_t* prol_bar = empty_bar + kMaxStages;
+    uint64_t* cols_ready = prol_bar + 1;
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + v.misc);
+    unsigned char* area = smem + v.area;
+    const uint32_t area_bytes = p.smem_window - v.area;  // p.smem_window: usable dynamic bytes
+    const uint32_t scratch_bytes = v2_scratch_bytes(P, Lt);
+    unsigned char* scratch = area + ((area_bytes - scratch_bytes) & ~15u);
+    const bool compact = p.compact != 0;
+
+    WorkList wl;
+    wl.sl = reinterpret_cast<uint32_t*>(smem + v.sl);
+    wl.slen = reinterpret_cast<uint32_t*>(smem + v.slen);
+    wl.sstart = reinterpret_cast<uint32_t*>(smem + v.sstart);
+    wl.cnt = reinterpret_cast<uint32_t*>(smem + v.cnt);
+    wl.pcols = reinterpret_cast<uint32_t*>(smem + v.pcols);
+    {
+        unsigned char* q = scratch;
+        wl.rel = reinterpret_cast<uint32_t*>(q);
+        q = align16(q, 4ull * (P + 1));
+        wl.raw = reinterpret_cast<uint16_t*>(q);
+        q = align16(q, 2ull * Lt + 32);
+        wl.wh = reinterpret_cast<uint32_t*>(q);
+        wl.hist = wl.wh + kLenBuckets * ((P + 31) / 32);
+        wl.hpad = wl.hist + kLenBuckets;
+        wl.wsum = wl.hpad + kLenBuckets;
+    }
+    const uint32_t* cdesc = reinterpret_cast<const uint32_t*>(smem + v.cdesc);
+    const uint16_t* ucols = reinterpret_cast<const uint16_t*>(smem + v.ucols);
+    uint32_t* acc = reinterpret_cast<uint32_t*>(smem + v.acc);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    unsigned long long* stamp = p.phase_ns ? p.phase_ns + 8ull * blockIdx.x : nullptr;
+    if (stamp && threadIdx.x == 0) stamp[0] = global_ns();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMaxStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], NCW);
+        }
+        mbar_init(prol_bar, 1);
+        mbar_init(cols_ready, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const uint32_t n_chunks = (P + CHUNK - 1) / CHUNK;
+    const uint32_t G = gridDim.x;
+    const uint32_t full = (p.n_tiles / G) * G;
+    const uint32_t rem = p.n_tiles - full;
+    uint32_t parts = rem ? G / rem : 1u;
+    parts = max(1u, min(parts, min(p.max_parts, n_chunks)));
+    const uint32_t n_items = full + rem * parts;
+
+    if (warp >= NCW) {
+        // ---------------- producer warps ----------------
+        const int pw = warp - NCW;
+        if (pw == 0 && lane == 1 && p.fitness_out && p.table_n) {
+            const uint64_t bytes = p.table_n * sizeof(double);
+            const uint64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 127) & ~uint64_t(127);
+            const uint64_t lo = per * blockIdx.x;
+            if (lo < bytes) {
+                const uint32_t n = static_cast<uint32_t>(min(per, bytes - lo) & ~uint64_t(15));
+                if (n) {
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     reinterpret_cast<const unsigned char*>(p.logt) + lo), "r"(n) : "memory");
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     reinterpret_cast<const unsigned char*>(p.expt) + lo), "r"(n) : "memory");
+                }
+            }
+        }
+        const unsigned char* ranks = p.ranks;
+        const size_t block_bytes = size_t(p.n_cols) * 128u;
+        const uint32_t scratch_at = static_cast<uint32_t>(scratch - area);
+        const uint32_t full_addr0 = smem_u32(&full_bar[0]);
+        const uint32_t area_addr = smem_u32(area);
+        if (!compact) {
+            // whole tiles: one contiguous block per tile, one thread
+            if (pw == 0 && lane == 0 && p.debug_mode != 3) {
+                const uint32_t stage_bytes = static_cast<uint32_t>(block_bytes), stages = p.stages;
+                uint32_t st = 0, phase = 0, issued = 0;
+                for (uint32_t item = blockIdx.x; item < n_items; item += G, ++issued) {
+                    const uint32_t tile = item < full ? item : full + (item - full) / parts;
+                    if (issued < stages && (st + 1) * stage_bytes > scratch_at) mbar_wait(prol_bar, 0);
+                    mbar_wait(&empty_bar[st], phase ^ 1u);
+                    if (p.debug_mode == 2) {
+                        mbar_arrive(&full_bar[st]);
+                    } else {
+                        mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                area_addr + st * stage_bytes),
+                            "l"(ranks + size_t(tile) * block_bytes), "r"(stage_bytes), "r"(full_addr0 + st * 8u)
+                            : "memory");
+                    }
+                    if (++st == stages) st = 0, phase ^= 1u;
+                }
+            }
+        } else {
+            if (p.host_cbf) {  // the CBF is copied in by CTA 0's consumers (stage_host_cbf)
+                if (pw == 0 && lane == 0) {
+                    uint32_t x;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(p.cbf_ready) : "memory");
+                    } while (x != p.cbf_seq);
+                }
+                named_bar_sync(2, kV2Producers * 32);
+            }
+            v2_build_columns(p, smem, v, pw, lane);
+            if (pw == 0 && lane == 0) {
+                const uint32_t sb = misc[0] * 128u;
+                uint32_t n = sb ? min(static_cast<uint32_t>(kV2MaxStages), area_bytes / sb) : 1u;
+                if (p.stages && p.stages < n) n = p.stages;  // EBIC_STAGES cap
+                misc[2] = max(n, 1u);
+                mbar_arrive(cols_ready);  // release: misc, runs, ucols, bm, bases
+            }
+            mbar_wait(cols_ready, 0);
+            const uint32_t stage_bytes = misc[0] * 128u;
+            const uint32_t stages = misc[2];
+            const uint32_t n_runs = misc[1];
+            const uint32_t* runs = reinterpret_cast<const uint32_t*>(smem + v.runs);
+            const uint32_t* run_slot = reinterpret_cast<const uint32_t*>(smem + v.run_slot);
+            // Copies issued by all producer lanes.  (A bulk copy takes uniform
+            // operands, so a warp issues its lanes' copies one after another;
+            // four warps keep enough in flight -- one thread alone is ~4x
+            // slower, tools/probes/gather_probe.cu modes 8/9.)
+            const uint32_t ptid = pw * 32 + lane;
+            uint32_t st = 0, phase = 0, issued = 0;
+            if (p.debug_mode != 3) {
+                for (uint32_t item = blockIdx.x; item < n_items; item += G, ++issued) {
+                    const uint32_t tile = item < full ? item : full + (item - full) / parts;
+                    if (ptid == 0) {  // one thread waits; the others sleep in the named barrier
+                        if (issued < stages && (st + 1) * stage_bytes > scratch_at) mbar_wait(prol_bar, 0);
+                        mbar_wait(&empty_bar[st], phase ^ 1u);
+                        if (p.debug_mode == 2) mbar_arrive(&full_bar[st]);
+                        else mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
+                    }
+                    named_bar_sync(2, kV2Producers * 32);
+                    if (p.debug_mode != 2) {
+                        const uint32_t dst = area_addr + st * stage_bytes;
+                        const uint32_t bar = full_addr0 + st * 8u;
+                        const unsigned char* srcb = ranks + size_t(tile) * block_bytes;
+                        for (uint32_t r = ptid; r < n_runs; r += kV2Producers * 32) {
+                            const uint32_t x = runs[r];
+                            asm volatile(
+                                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                                    dst + run_slot[r] * 128u),
+                                "l"(srcb + size_t(x >> 16) * 128u), "r"((x & 0xffffu) * 128u), "r"(bar)
+                                : "memory");
+                        }
+                    }
+                    if (++st == stages) st = 0, phase ^= 1u;
+                }
+            }
+        }
+    } else {
+        // ---------------- consumer warps ----------------
+        if (p.host_cbf) stage_host_cbf(p, threadIdx.x, NCW * 32, 1);
+        v2_build_work_list<CHUNK>(p, smem, v, wl, compact ? cols_ready : nullptr, threadIdx.x, NCW * 32, 1);
+        if (threadIdx.x == 0) mbar_arrive(prol_bar);
+        if (stamp && threadIdx.x == 0) stamp[1] = global_ns();
+        const uint32_t stages = compact ? misc[2] : p.stages;
+        const uint32_t stage_bytes = compact ? misc[0] * 128u : p.n_cols * 128u;
+
+        // rows the collapsed layout cannot represent, evaluated in fp64 (see v1)
+        for (uint32_t i = G - 1 - blockIdx.x; i < p.n_excl; i += G) {
+            const double* rowv = p.excl_vals + size_t(i) * p.n_cols;
+            for (uint32_t g = threadIdx.x; g < P; g += NCW * 32) {
+                const uint32_t len = wl.slen[g];
+                const uint32_t* pc = wl.pcols + wl.sstart[g];
+                auto col = [&](uint32_t off) -> uint32_t { return compact ? ucols[off >> 7] : (off >> 7); };
+                bool ok = true;
+                if (len > 1) {
+                    double prev = __ldg(rowv + col(pc[0]));
+                    for (uint32_t k = 1; k < len; ++k) {
+                        const double cur = __ldg(rowv + col(pc[k]));
+                        ok = ok & step_ok<false>(prev, cur, p.eps);
+                        prev = cur;
+                    }
+                }
+                if (ok) atomicAdd(&wl.cnt[g], 1u);
+            }
+        }
+
+        const int grp = lane / GL;
+        const int gl = lane % GL;
+        const typename W::Mask all_valid = W::valid(0, 0xffffffffu, 0u, p.rank_k);
+        const uint32_t area_addr = smem_u32(area) + gl * 16u;
+        uint32_t st = 0, phase = 0;
+        for (uint32_t item = blockIdx.x; item < n_items; item += G) {
+            uint32_t tile = item, c_lo = 0, c_hi = n_chunks;
+            if (item >= full) {  // a part of a last-wave tile: a chunk range
+                const uint32_t j = item - full, part = j % parts;
+                tile = full + j / parts;
+                c_lo = part * n_chunks / parts;
+                c_hi = (part + 1) * n_chunks / parts;
+            }
+            const uint32_t r0 = tile * RPG + gl * RPL;
+            uint32_t excl = 0;
+            if (p.row_excl) excl = static_cast<uint32_t>(__ldg(p.row_excl + (r0 >> 6)) >> (r0 & 63)) & ((1u << RPL) - 1u);
+            if (p.debug_mode != 3) mbar_wait(&full_bar[st], phase);
+            const uint32_t base = area_addr + st * stage_bytes;
+            typename W::Mask vm = all_valid;
+            if ((tile + 1) * RPG > p.n_rows || excl != 0u) vm = W::valid(r0, p.n_rows, excl, p.rank_k);
+
+            if (p.debug_mode != 1) {
+                // Chunks longest first, statically: warp w takes the k-th
+                // longest for k = (w + 7 item) mod NCW + j NCW; the rotation
+                // evens each warp's share out over the tiles.  Each lane adds
+                // its own partial counts (16-bit halves: q = 0, 1) to a private
+                // word of the chunk -- no shuffles, no contended atomics.
+                const uint32_t n_here = c_hi - c_lo;
+                for (uint32_t k = (static_cast<uint32_t>(warp) + item * 7u) % NCW; k < n_here; k += NCW) {
+                    const uint32_t ch = c_hi - 1 - k;
+                    const uint32_t d = cdesc[ch];
+                    uint32_t c;
+                    if (d) {
+                        const uint32_t len = d & 0xffu;
+                        const uint32_t stride = pad4(len);
+                        c = v2_count_uniform<W>(len, base, wl.pcols + (d >> 8) + grp * SPG * stride, stride, vm);
+                    } else {
+                        const uint32_t g0 = ch * CHUNK + grp * SPG;
+                        c = 0;
+#pragma unroll
+                        for (int q = 0; q < SPG; ++q)
+                            if (g0 + q < P)
+                                c |= W::count_any(base, wl.pcols + wl.sstart[g0 + q], wl.slen[g0 + q], vm) << (16 * q);
+                    }
+                    if (c) atomicAdd(&acc[ch * 32 + lane], c);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[st]);
+            if (++st == stages) st = 0, phase ^= 1u;
+        }
+    }
+    __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[2] = global_ns();
+    {
+        // sum each chunk's per-lane words over its groups' lanes
+        const int nwarps = blockDim.x >> 5;
+        const int grp = lane / GL, gl = lane % GL;
+        for (uint32_t ch = warp; ch < n_chunks; ch += nwarps) {
+            uint32_t x = acc[ch * 32 + lane];
+#pragma unroll
+            for (int o = GL / 2; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            const uint32_t g0 = ch * CHUNK + grp * SPG;
+            if (gl == 0) {
+                if (g0 < P) wl.cnt[g0] += x & 0xffffu;  // + the fp64 fix-up rows
+                if (g0 + 1 < P) wl.cnt[g0 + 1] += x >> 16;
+            }
+        }
+        __syncthreads();
+    }
+    count_epilogue(p, wl.cnt, wl.sl);
+    if (stamp && threadIdx.x == 0) stamp[3] = global_ns();
+}
+
+}  // namespace ebic_b200

@@ -14,7 +14,7 @@ import pytest
 
 import oracle
 import paper_1801_03039_b200 as eb
-from golden_io import TRACE_NAMES, acceptance, expansion_cases, fitness_trials, trace
+from golden_io import STEADY_NAMES, TRACE_NAMES, acceptance, expansion_cases, fitness_trials, trace
 
 pytestmark = pytest.mark.gpu
 port = oracle.Port()
@@ -27,7 +27,10 @@ KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NCW="24"), dict(EBIC_N
                    dict(EBIC_SPG="4", EBIC_NO_COLLAPSE="1")] +
                   [dict(EBIC_LAYOUT_F64="1", EBIC_RPG=str(g), EBIC_RPL=str(l))
                    for g in (32, 16, 8, 4) for l in (1, 2)] +
-                  [dict(EBIC_LAYOUT_F64="1", EBIC_NCW="16"), dict(EBIC_LAYOUT_F64="1", EBIC_NCW="32"), dict(EBIC_FORCE_DIRECT="1")])
+                  [dict(EBIC_LAYOUT_F64="1", EBIC_NCW="16"), dict(EBIC_LAYOUT_F64="1", EBIC_NCW="32"), dict(EBIC_FORCE_DIRECT="1")] +
+                  # K1v2 (default for rank layouts) vs the v1 tile kernel, and K1v2's own knobs
+                  [dict(EBIC_KERNEL="1"), dict(EBIC_KERNEL="1", EBIC_NO_COLLAPSE="1"), dict(EBIC_COMPACT="1"), dict(EBIC_COMPACT="0"),
+                   dict(EBIC_COMPACT="1", EBIC_GAP="2"), dict(EBIC_STAGES="1"), dict(EBIC_COMPACT="1", EBIC_NO_COLLAPSE="1")])
 
 
 @contextmanager
@@ -88,7 +91,7 @@ def test_fitness_trials_golden():  # test_fitness.cpp:111-137
             assert (ev.count_matches(eb.CbfPopulation(off, cols), eps) == counts).all()
 
 
-@pytest.mark.parametrize("name", TRACE_NAMES)
+@pytest.mark.parametrize("name", TRACE_NAMES + STEADY_NAMES)
 def test_trace_golden(name):
     """Every batch of a recorded reference GA run: counts and fitness bit-exact."""
     t = trace(name)
@@ -156,6 +159,44 @@ def test_edge_cases_vs_oracle(cfg):
                     got = ev.count_matches(pop, eps)
                     want = port.count_matches(v, pop.offsets, pop.col_indices, eps)
                     assert (got == want).all(), (rows, n_cols, eps)
+
+
+V2_CONFIGS = [dict(), dict(EBIC_NO_COLLAPSE="1"), dict(EBIC_COMPACT="1"), dict(EBIC_COMPACT="0"),
+              dict(EBIC_COMPACT="1", EBIC_GAP="1"), dict(EBIC_COMPACT="1", EBIC_GAP="2"),
+              dict(EBIC_COMPACT="1", EBIC_NO_COLLAPSE="1"), dict(EBIC_STAGES="1"), dict(EBIC_COMPACT="1", EBIC_STAGES="1"),
+              dict(EBIC_GRID="7"), dict(EBIC_COMPACT="1", EBIC_GRID="7")]
+
+
+@pytest.mark.parametrize("cfg", V2_CONFIGS, ids=lambda d: "-".join(f"{k}={v}" for k, v in d.items()) or "default")
+def test_v2_column_runs_vs_oracle(cfg):
+    """K1v2 stages only the launch's referenced columns, as runs of consecutive
+    columns: every column (one run, a 1000-column stage that fits only once),
+    every other column (the most runs), the two edge columns, one tail block,
+    a single repeated column, and random sets -- over 1 tile and many."""
+    rng = np.random.default_rng(21)
+    n_cols = 1000
+    pops = {
+        "all": [list(map(int, rng.permutation(n_cols)[:8])) for _ in range(40)] +
+               [list(range(k, n_cols, 125)) for k in range(125)],
+        "every_other": [list(map(int, rng.choice(np.arange(0, n_cols, 2), size=int(rng.integers(2, 9)),
+                                                 replace=False))) for _ in range(300)] +
+                       [list(range(k, n_cols, 250)) for k in range(0, 250, 2)],
+        "edges": [[0, n_cols - 1], [n_cols - 1, 0]] * 20,
+        "tail": [list(map(int, rng.choice(np.arange(n_cols - 64, n_cols), size=int(rng.integers(2, 12)),
+                                          replace=False))) for _ in range(200)],
+        "one_col": [[5, 5, 5], [5, 5]] * 9,
+        "random": random_population(rng, n_cols, 700, max_len=14),
+    }
+    with env(**cfg):
+        for rows in (700, 13000):
+            v = np.round(rng.standard_normal((rows, n_cols)), 2)
+            with eb.Evaluator(v) as ev:
+                for name, series in pops.items():
+                    pop = cbf(series)
+                    for eps in (0.0, 1e-9, 0.05):
+                        got = ev.count_matches(pop, eps)
+                        want = port.count_matches(v, pop.offsets, pop.col_indices, eps)
+                        assert (got == want).all(), (rows, name, eps)
 
 
 def test_empty_population_and_errors():
@@ -310,7 +351,7 @@ def test_finalize_biclusters_c4_top_series():
     m = eb.ExpressionMatrix(v)
     out = eb.finalize_biclusters(entries, m, eb.ExpansionOptions(), t.eps, 0.0)
     assert len(out) == 100
-    for b in out[:12]:
+    for b in out:  # every finalized bicluster
         core = port.assign_rows(v, b.series, t.eps)
         wr, wf = port.expand_bicluster(v, b.series, core, [0] * len(core), True, 1, t.eps)
         assert b.rows == wr and [int(f) for f in b.row_flags] == wf

@@ -31,9 +31,23 @@ def main():
 
     name = sys.argv[1]
     variants = sys.argv[2:] or [""]
-    t = trace(name)
-    batches = t.steady_batches() if name.endswith("ss") else t.batches
-    values = t.matrix()
+    if name.startswith("synth:"):
+        # synth:ROWS,COLS,P,LEN -- N(0,1) matrix, P random series of LEN columns
+        # (no reference counts: parity is not checked)
+        R, Cc, P, L = map(int, name[6:].split(","))
+        rng = np.random.default_rng(11)
+        values = rng.standard_normal((R, Cc))
+        cols = np.concatenate([rng.choice(Cc, size=L, replace=False) for _ in range(P)]).astype(np.uint16)
+        off = np.arange(P + 1, dtype=np.uint64) * L
+
+        class T:
+            eps, sigma = 1e-9, max(4, -(-R // 50))
+        t = T()
+        batches = [(off, cols, None, None)]
+    else:
+        t = trace(name)
+        batches = t.steady_batches() if name.endswith("ss") else t.batches
+        values = t.matrix()
     dev = torch.device("cuda", 0)
     stream = torch.cuda.Stream(dev)
     torch.cuda.set_stream(stream)
@@ -64,7 +78,7 @@ def main():
             step(b)
         torch.cuda.synchronize()
         parity = None
-        if os.environ.get("EBIC_DEBUG_MODE", "0") == "0":
+        if os.environ.get("EBIC_DEBUG_MODE", "0") == "0" and bs[0]["want"][0] is not None:
             parity = True
             for b in bs:
                 step(b)
