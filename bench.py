@@ -58,17 +58,28 @@ METRIC = "biclusters evaluated/sec"
 UNIT = "biclusters/s"
 
 WORKLOADS = {
-    # name: trace fixture (holds the scenario spec, eps and the reference batches)
-    "c4": "c4",
-    "c5": "c5",
-    "c3": "c3",
-    "c1": "c1e",
+    # name: (trace fixture, first generation replayed).  C4 / C5 replay the
+    # steady state of long reference runs (tests/golden/make_golden.py STEADY:
+    # C4 generations 250..5000 of 5000, every 250th; C5 generations 100..1000
+    # of 1000, every 100th); "c4early" / "c5early" the first generations.
+    "c4": ("c4ss", 250),
+    "c5": ("c5ss", 50),
+    "c4early": ("c4", 0),
+    "c5early": ("c5", 0),
+    "c3": ("c3", 0),
+    "c1": ("c1e", 0),
 }
 
 
 def load_workload(name: str):
+    import copy
     from golden_io import trace
-    t = trace(WORKLOADS[name])
+    tname, min_gen = WORKLOADS[name]
+    t = copy.copy(trace(tname))
+    if min_gen:
+        keep = [g >= min_gen for g in t.generations]
+        t.batches = [b for b, k in zip(t.batches, keep) if k]
+        t.generations = [g for g, k in zip(t.generations, keep) if k]
     return t
 
 
@@ -233,9 +244,12 @@ def run_reference_arm(args):
 
 def workload_config(t, args, world=1, devices=1):
     s = t.spec
+    gens = list(getattr(t, "generations", []))
     return {"workload": f"{args.workload}: synthetic {s['rows']}x{s['cols']} "
                         f"({len(s['blocks'])} planted {s['blocks'][0][0]}x{s['blocks'][0][1]} trend blocks, "
-                        f"seed {s['seed']}), reference GA novel batches (population 600)",
+                        f"seed {s['seed']}), reference GA novel batches (population 600)"
+                        + (f", generations {gens[0]}..{gens[-1]} of a {t.iterations}-generation run"
+                           if gens else ""),
             "rows": s["rows"], "cols": s["cols"],
             "series_per_step": round(float(np.mean([len(b[0]) - 1 for b in t.batches])), 1),
             "eps": t.eps, "sigma": t.sigma, "l2": "evicted between timed steps (512 MB read, outside the timed events)",
@@ -337,8 +351,7 @@ def large_roofline(args, peak, evict, sharded=False, world=1, rank=0, backend="n
                    "parity": "counts and fitness bit-exact vs the reference trace on every batch"}
     if sharded:
         ev.close()
-        return {"workload": "c5: synthetic 200000x1000 (5 planted 6000x30 trend blocks, seed 2026+1), "
-                            "reference GA batches", "row_sharded": row_sharded}
+        return {"workload": C5_DESC, "row_sharded": row_sharded}
 
     nbytes = 0
     steps = max(20, min(args.steps // 20, 200))
@@ -354,13 +367,13 @@ def large_roofline(args, peak, evict, sharded=False, world=1, rank=0, backend="n
     us = e0.elapsed_time(e1) * 1e3 / steps
     series = sum(bs[k % len(bs)]["P"] for k in range(steps))
     achieved = nbytes / steps / (us / 1e6) / 1e9
-    # The kernel stages whole row tiles (every column, read once): the DRAM
-    # bytes it actually moves per launch, against the algorithmic bytes above
-    # (only the columns some series uses).
-    staged = R * ev.n_cols * LAYOUT_CELL_BYTES[layout]
+    # Bytes the kernel stages per launch: K1v2 at this size copies only the
+    # launch's referenced columns (= the algorithmic matrix bytes); the v1
+    # kernel (EBIC_KERNEL=1) stages whole row tiles.
+    staged = (nbytes / steps if os.environ.get("EBIC_KERNEL", "2") != "1"
+              else R * ev.n_cols * LAYOUT_CELL_BYTES[layout])
     ev.close()
-    return {"workload": "c5: synthetic 200000x1000 (5 planted 6000x30 trend blocks, seed 2026+1), "
-                        "reference GA batches", "bound": "hbm", "achieved": achieved, "peak": peak,
+    return {"workload": C5_DESC, "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": achieved / peak, "avg_launch_us": us,
             "algorithmic_bytes_per_launch": nbytes / steps, "layout": LAYOUT_NAMES[layout],
             "staged_bytes_per_launch": staged,
@@ -368,6 +381,10 @@ def large_roofline(args, peak, evict, sharded=False, world=1, rank=0, backend="n
             "biclusters_per_s": series / (us * steps / 1e6), "steps": steps,
             "timing": "back-to-back launches between one CUDA event pair (inputs > L2)",
             "row_sharded": row_sharded}
+
+
+C5_DESC = ("c5: synthetic 200000x1000 (5 planted 6000x30 trend blocks, seed 2027), reference GA "
+           "batches of generations 100..1000 (every 100th) of a 1000-generation run")
 
 
 def run_e2e_driver(t, args):
@@ -784,7 +801,8 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4",
+                    help="c4: BASELINE config 4, steady-state GA batches (default); c5: config 5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-large", action="store_true",
                     help="skip the config-5 (200,000 x 1000) roofline run")

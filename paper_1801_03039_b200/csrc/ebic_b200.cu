@@ -299,10 +299,11 @@ void grow_pinned(unsigned char** p, size_t* cap, size_t need) {
 
 // Reduction scratch of one count launch: striped accumulators [P][kStripes]
 // (zero between launches) or the tree's (grid + groups) rows of P counters.
-void ensure_partial(Shard& s, size_t P, int grid, bool striped) {
+// mode: 0 tree, 1 u32 stripes [P][8], 2 fp32 stripes [8][P rounded to 4] (K1v2)
+void ensure_partial(Shard& s, size_t P, int grid, int mode) {
     const size_t gsz = reduce_group_size((uint32_t)grid);
-    const size_t need = striped ? P * kStripes : (size_t(grid) + (grid + gsz - 1) / gsz) * P;
-    const int mode = striped ? 1 : 0;
+    const size_t need = mode == 2 ? ((P + 3) & ~size_t(3)) * kStripes
+                        : mode == 1 ? P * kStripes : (size_t(grid) + (grid + gsz - 1) / gsz) * P;
     if (need <= s.partial_cap && mode == s.last_reduce) return;
     // a launch still queued on the previous stream may use the old scratch
     if (s.cur_stream) CK(cudaStreamSynchronize(s.cur_stream));
@@ -984,8 +985,9 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         p.smem_window = (uint32_t)(smem - 128);
         int grid = std::min<int>((int)p.n_tiles, s.sm_count);
         if (s.knobs.grid > 0) grid = std::min<int>(s.knobs.grid, (int)p.n_tiles);
-        // per-CTA counts in 16-bit halves while a CTA's rows fit
         p.gap = (uint32_t)std::min(std::max(s.knobs.gap, 0), 2);
+        // 4-wide fp32 stripe reductions while every count is exact in fp32
+        if (p.reduce_striped && s.rows < (1u << 24)) p.reduce_striped = 2;
         // Whole tiles (one contiguous copy each, issued at once) for short
         // launches; the referenced columns only once a CTA walks enough tiles
         // to amortise building the column set first, or when two whole-tile
@@ -1004,7 +1006,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         s.last_grid = grid;
         s.last_cfg = c;
         s.last_collapsed = rl->collapsed;
-        ensure_partial(s, P, grid, p.reduce_striped != 0);
+        ensure_partial(s, P, grid, (int)p.reduce_striped);
         p.partial = s.d_partial;
         if (rl->collapsed) {
             p.rank_k = 0x80008000u;
@@ -1051,7 +1053,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         s.last_grid = grid;
         s.last_cfg = c;
         s.last_collapsed = c.layout && rl->collapsed;
-        ensure_partial(s, P, grid, p.reduce_striped != 0);
+        ensure_partial(s, P, grid, (int)p.reduce_striped);
         p.partial = s.d_partial;
         if (c.layout && rl->collapsed) {
             p.rank_k = 0x80008000u;
@@ -1075,7 +1077,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         s.last_grid = grid;
         s.last_cfg = c;
         s.last_collapsed = false;
-        ensure_partial(s, P, grid, p.reduce_striped != 0);
+        ensure_partial(s, P, grid, (int)p.reduce_striped);
         p.partial = s.d_partial;
         if (e0) {
             CK(cudaFuncSetAttribute(count_direct_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

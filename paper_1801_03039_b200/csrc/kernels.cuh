@@ -579,6 +579,60 @@ __device__ __forceinline__ void count_epilogue_striped(const CountParams& p, con
     signal_done(p);
 }
 
+// Striped tail with 4-wide float reductions (reduce_striped == 2, K1v2):
+// `by_series` holds this CTA's counts indexed by series.  Counts are integers
+// below 2^24 (the host requires shard rows < 2^24), so fp32 adds are exact;
+// one red.global.add.v4.f32 carries four series (a quarter of the L2 atomic
+// operations of the u32 stripes).  Accumulator: [kStripes][P4] floats, P4 =
+// P rounded up to 4, zero between launches.
+__device__ __forceinline__ void count_epilogue_v4(const CountParams& p, const uint32_t* by_series) {
+    const uint32_t P = p.n_series, P4 = (P + 3u) & ~3u;
+    float* acc = reinterpret_cast<float*>(p.partial);
+    const uint32_t stripe = blockIdx.x % kStripes;
+    unsigned long long* stamp = p.phase_ns ? p.phase_ns + 8ull * blockIdx.x : nullptr;
+    __shared__ int s_last;
+    for (uint32_t i = threadIdx.x; i < P4 / 4; i += blockDim.x) {
+        const uint4 c = *reinterpret_cast<const uint4*>(by_series + 4 * i);
+        if (c.x | c.y | c.z | c.w)
+            asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
+                             acc + size_t(stripe) * P4 + 4 * i),
+                         "f"(static_cast<float>(c.x)), "f"(static_cast<float>(c.y)), "f"(static_cast<float>(c.z)),
+                         "f"(static_cast<float>(c.w))
+                         : "memory");
+    }
+    __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[4] = global_ns();
+    if (threadIdx.x == 0) s_last = ticket_acq_rel(&p.done[kMaxGroups]) == gridDim.x - 1;
+    __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[5] = global_ns();
+    if (!s_last) return;
+    if (stamp && threadIdx.x == 0) stamp[7] = global_ns();
+    for (uint32_t s = threadIdx.x; s < P; s += blockDim.x) {
+        float x[kStripes];
+#pragma unroll
+        for (int k = 0; k < kStripes; ++k) x[k] = __ldcg(acc + size_t(k) * P4 + s);
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < kStripes; ++k) t += static_cast<double>(x[k]);
+#pragma unroll
+        for (int k = 0; k < kStripes; ++k) __stcg(acc + size_t(k) * P4 + s, 0.0f);
+        const uint64_t c = static_cast<uint64_t>(t);
+        if (p.xacc) {
+            if (c) atomicAdd_system(p.xacc + s, static_cast<unsigned long long>(c));
+            continue;
+        }
+        p.counts_out[s] = c;
+        if (p.fitness_out)
+            p.fitness_out[s] = fitness_from_tables(c, p.offsets[s + 1] - p.offsets[s], p.sigma, p.logt, p.expt);
+    }
+    if (threadIdx.x == 0) p.done[kMaxGroups] = 0u;
+    if (p.xacc) {
+        cross_shard_finish(p);
+        return;
+    }
+    signal_done(p);
+}
+
 __device__ __forceinline__ void count_epilogue(const CountParams& p, const uint32_t* s_cnt,
                                                const uint32_t* slot_series) {
     if (p.reduce_striped) {
@@ -976,25 +1030,44 @@ struct RankWalker {
 
 // Host-resident CBF (see CountParams::host_cbf): CTA 0's consumers copy it
 // into device memory with one round of 16-byte PCIe reads and publish a
-// release flag; every other CTA acquires it.  CTAs are launched in index
-// order, so CTA 0 is resident whenever another CTA waits here.
+// release flag; every other CTA acquires it.  CTA 0 is normally resident
+// first (CTAs start in index order), but nothing guarantees it -- with more
+// CTAs than free SMs, or SMs held by another process -- so a CTA that has
+// waited 20 us copies the (identical) bytes itself: forward progress never
+// depends on another CTA being scheduled.
 __device__ __forceinline__ void stage_host_cbf(const CountParams& p, int tid, int nthreads,
                                                int bar_id) {
+    __shared__ int s_self;
     if (blockIdx.x == 0) {
         for (uint32_t i = tid; i < p.cbf_words; i += nthreads) p.dev_cbf[i] = p.host_cbf[i];
         __threadfence();
         named_bar_sync(bar_id, nthreads);
-        if (tid == 0)
+        // (EBIC_DEBUG_MODE=4, tests only: CTA 0 never publishes, so every
+        // other CTA takes the self-copy path)
+        if (tid == 0 && p.debug_mode != 4)
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p.cbf_ready), "r"(p.cbf_seq)
                          : "memory");
     } else {
         if (tid == 0) {
+            const unsigned long long t0 = global_ns();
             uint32_t v;
-            do {
+            int self = 0;
+            for (;;) {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.cbf_ready) : "memory");
-            } while (v != p.cbf_seq);
+                if (v == p.cbf_seq) break;
+                if (global_ns() - t0 > 20000ull) {
+                    self = 1;
+                    break;
+                }
+            }
+            s_self = self;
         }
         named_bar_sync(bar_id, nthreads);
+        if (s_self) {
+            for (uint32_t i = tid; i < p.cbf_words; i += nthreads) p.dev_cbf[i] = p.host_cbf[i];
+            __threadfence();
+            named_bar_sync(bar_id, nthreads);
+        }
     }
 }
 

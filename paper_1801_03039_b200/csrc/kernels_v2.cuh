@@ -36,6 +36,7 @@ constexpr int kV2Producers = 4;     // producer warps (bulk-copy issue is per la
 constexpr int kV2MaxCols = 2048;    // bitmap of 64 words
 constexpr int kV2Chunk = 8;         // slots per warp iteration (4 groups x 2 series)
 constexpr int kV2MaxStages = 4;
+constexpr uint32_t kV2ExclItems = 64;  // per-CTA items whose excl words are preloaded
 
 // Byte offsets of the persistent work list inside the dynamic window.
 struct V2Layout {
@@ -47,7 +48,8 @@ struct V2Layout {
     uint32_t bm, bases; // u32[64] each
     uint32_t ucols;     // u16[n_cols] slot -> column
     uint32_t runs, run_slot;  // u32[max_runs] each
-    uint32_t acc;       // u32[n_chunks][32] per-lane partial counts (owned schedule)
+    uint32_t acc;       // u32[n_chunks][32] per-lane partial counts
+    uint32_t excl;      // u64[kV2ExclItems] excl words of the CTA's items
     uint32_t area;      // first byte of the stage area (128-aligned)
 };
 
@@ -73,6 +75,7 @@ __host__ __device__ inline V2Layout v2_layout(uint32_t P, uint32_t L, uint32_t n
     v.runs = at;     at = up16(at + 4 * v2_max_runs(n_cols));
     v.run_slot = at; at = up16(at + 4 * v2_max_runs(n_cols));
     v.acc = at;      at = up16(at + 4 * 32 * ((P + kV2Chunk - 1) / kV2Chunk));
+    v.excl = at;     at = up16(at + 8 * kV2ExclItems);
     v.area = (at + 127u) & ~127u;
     return v;
 }
@@ -267,6 +270,12 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
     }
     for (uint32_t i = tid; i < nblk * kLenBuckets; i += nthreads) w.wh[i] = 0;
     for (int b = tid; b < kLenBuckets; b += nthreads) w.hist[b] = 0;
+    for (uint32_t i = tid; i < P + 2; i += nthreads) w.cnt[i] = 0;
+    {
+        uint32_t* acc = reinterpret_cast<uint32_t*>(smem + v.acc);
+        const uint32_t n_acc = 32u * ((P + CHUNK - 1) / CHUNK);
+        for (uint32_t i = tid; i < n_acc; i += nthreads) acc[i] = 0;
+    }
     named_bar_sync(bar_id, nthreads);  // 1
 
     auto bucket_of = [&](uint32_t s, uint32_t& len) -> uint32_t {
@@ -321,16 +330,19 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
         if (bkt < kLenBuckets - 1) {
             const uint32_t st = w.hpad[bkt] + r * pad4(len);
             w.sstart[g] = st;
+            if (g % CHUNK == 0) {
+                // chunk descriptor: (first list entry << 8) | length when the
+                // whole chunk lies in this length's bucket (lists consecutive,
+                // stride pad4(length)) and the length is unrolled (2..12); else
+                // 0 (per-slot path).  Bucket b ends where bucket b + 1 starts.
+                const uint32_t end = w.hist[bkt + 1];
+                const bool uni = g + CHUNK <= end && len >= 2 && len <= 12;
+                reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = uni ? ((st << 8) | len) : 0u;
+            }
             const uint16_t* from = w.raw + w.rel[s];
             for (uint32_t i = 0; i < pad4(len); ++i)
                 w.pcols[st + i] = i < len ? slot_of(from[i]) * 128u : 0u;
         }
-    }
-    for (uint32_t i = tid; i < P + 2; i += nthreads) w.cnt[i] = 0;
-    {
-        uint32_t* acc = reinterpret_cast<uint32_t*>(smem + v.acc);
-        const uint32_t n_acc = 32u * ((P + CHUNK - 1) / CHUNK);
-        for (uint32_t i = tid; i < n_acc; i += nthreads) acc[i] = 0;
     }
     named_bar_sync(bar_id, nthreads);  // 4
 
@@ -351,17 +363,10 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
                 w.pcols[st + i] = i < len ? slot_of(from[i]) * 128u : 0u;
         }
     }
-    // chunk descriptors: (first list entry << 8) | length for a full chunk of
-    // one length in [2, 12] (its lists are consecutive, stride pad4(length)),
-    // else 0 (per-slot path)
+    // overflow-bucket chunks (lengths >= 63) take the per-slot path
     uint32_t* cdesc = reinterpret_cast<uint32_t*>(smem + v.cdesc);
-    const uint32_t n_chunks = (P + CHUNK - 1) / CHUNK;
-    for (uint32_t ch = tid; ch < n_chunks; ch += nthreads) {
-        const uint32_t first = ch * CHUNK;
-        const uint32_t l0 = w.slen[first];
-        const bool uni = first + CHUNK <= P && w.slen[first + CHUNK - 1] == l0 && l0 >= 2 && l0 <= 12;
-        cdesc[ch] = uni ? ((w.sstart[first] << 8) | l0) : 0u;
-    }
+    for (uint32_t ch = (ovf + CHUNK - 1) / CHUNK + tid; ch < (P + CHUNK - 1) / CHUNK; ch += nthreads) cdesc[ch] = 0u;
+    if (ovf % CHUNK && tid == 0) cdesc[ovf / CHUNK] = 0u;
     named_bar_sync(bar_id, nthreads);  // 5
 }
 
@@ -536,15 +541,9 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
                 }
             }
         } else {
-            if (p.host_cbf) {  // the CBF is copied in by CTA 0's consumers (stage_host_cbf)
-                if (pw == 0 && lane == 0) {
-                    uint32_t x;
-                    do {
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(p.cbf_ready) : "memory");
-                    } while (x != p.cbf_seq);
-                }
-                named_bar_sync(2, kV2Producers * 32);
-            }
+            // the host CBF is in device memory once this CTA's consumers are
+            // past stage_host_cbf (barrier 3: consumers + producers)
+            if (p.host_cbf) named_bar_sync(3, (NCW + kV2Producers) * 32);
             v2_build_columns(p, smem, v, pw, lane);
             if (pw == 0 && lane == 0) {
                 const uint32_t sb = misc[0] * 128u;
@@ -594,7 +593,13 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
         }
     } else {
         // ---------------- consumer warps ----------------
-        if (p.host_cbf) stage_host_cbf(p, threadIdx.x, NCW * 32, 1);
+        if (p.host_cbf) {
+            stage_host_cbf(p, threadIdx.x, NCW * 32, 1);
+            if (compact) {
+                __threadfence_block();
+                named_bar_sync(3, (NCW + kV2Producers) * 32);  // releases the producers (column set)
+            }
+        }
         v2_build_work_list<CHUNK>(p, smem, v, wl, compact ? cols_ready : nullptr, threadIdx.x, NCW * 32, 1);
         if (threadIdx.x == 0) mbar_arrive(prol_bar);
         if (stamp && threadIdx.x == 0) stamp[1] = global_ns();
@@ -626,7 +631,24 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
         const typename W::Mask all_valid = W::valid(0, 0xffffffffu, 0u, p.rank_k);
         const uint32_t area_addr = smem_u32(area) + gl * 16u;
         uint32_t st = 0, phase = 0;
-        for (uint32_t item = blockIdx.x; item < n_items; item += G) {
+        // excl words of this CTA's first kV2ExclItems items (rows the layout
+        // cannot represent), loaded once instead of a dependent global load
+        // per item right before its walk
+        unsigned long long* excl_items = reinterpret_cast<unsigned long long*>(smem + v.excl);
+        if (p.row_excl) {
+            for (uint32_t t = threadIdx.x; t < kV2ExclItems; t += NCW * 32) {
+                const uint32_t item = blockIdx.x + t * G;
+                unsigned long long w = 0ull;
+                if (item < n_items) {
+                    const uint32_t tl = item < full ? item : full + (item - full) / parts;
+                    w = __ldg(p.row_excl + ((tl * RPG) >> 6));
+                }
+                excl_items[t] = w;
+            }
+            named_bar_sync(1, NCW * 32);
+        }
+        uint32_t it = 0;  // this CTA's item number
+        for (uint32_t item = blockIdx.x; item < n_items; item += G, ++it) {
             uint32_t tile = item, c_lo = 0, c_hi = n_chunks;
             if (item >= full) {  // a part of a last-wave tile: a chunk range
                 const uint32_t j = item - full, part = j % parts;
@@ -636,7 +658,10 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
             }
             const uint32_t r0 = tile * RPG + gl * RPL;
             uint32_t excl = 0;
-            if (p.row_excl) excl = static_cast<uint32_t>(__ldg(p.row_excl + (r0 >> 6)) >> (r0 & 63)) & ((1u << RPL) - 1u);
+            if (p.row_excl) {
+                const unsigned long long w = it < kV2ExclItems ? excl_items[it] : __ldg(p.row_excl + (r0 >> 6));
+                excl = static_cast<uint32_t>(w >> (r0 & 63)) & ((1u << RPL) - 1u);
+            }
             if (p.debug_mode != 3) mbar_wait(&full_bar[st], phase);
             const uint32_t base = area_addr + st * stage_bytes;
             typename W::Mask vm = all_valid;
@@ -675,23 +700,29 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
     }
     __syncthreads();
     if (stamp && threadIdx.x == 0) stamp[2] = global_ns();
+    // Sum each chunk's per-lane words over its groups' lanes, add the fp64
+    // fix-up rows, and store the CTA's counts by series (the stage area is
+    // idle now) for the cross-CTA tail.
+    uint32_t* by_series = reinterpret_cast<uint32_t*>(area);
     {
-        // sum each chunk's per-lane words over its groups' lanes
         const int nwarps = blockDim.x >> 5;
         const int grp = lane / GL, gl = lane % GL;
+        for (uint32_t i = threadIdx.x; i < ((P + 3u) & ~3u); i += blockDim.x) by_series[i] = 0;
+        __syncthreads();
         for (uint32_t ch = warp; ch < n_chunks; ch += nwarps) {
             uint32_t x = acc[ch * 32 + lane];
 #pragma unroll
             for (int o = GL / 2; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
             const uint32_t g0 = ch * CHUNK + grp * SPG;
             if (gl == 0) {
-                if (g0 < P) wl.cnt[g0] += x & 0xffffu;  // + the fp64 fix-up rows
-                if (g0 + 1 < P) wl.cnt[g0 + 1] += x >> 16;
+                if (g0 < P) by_series[wl.sl[g0]] = wl.cnt[g0] + (x & 0xffffu);
+                if (g0 + 1 < P) by_series[wl.sl[g0 + 1]] = wl.cnt[g0 + 1] + (x >> 16);
             }
         }
         __syncthreads();
     }
-    count_epilogue(p, wl.cnt, wl.sl);
+    if (p.reduce_striped == 2) count_epilogue_v4(p, by_series);
+    else count_epilogue(p, by_series, nullptr);
     if (stamp && threadIdx.x == 0) stamp[3] = global_ns();
 }
 

@@ -199,6 +199,21 @@ def test_v2_column_runs_vs_oracle(cfg):
                         assert (got == want).all(), (rows, name, eps)
 
 
+@pytest.mark.parametrize("cfg", [dict(), dict(EBIC_COMPACT="1"), dict(EBIC_KERNEL="1")], ids=str)
+def test_host_cbf_staging_without_cta0(cfg):
+    """Host-buffer calls: the population is copied to the device by CTA 0 and
+    published with a flag.  EBIC_DEBUG_MODE=4 suppresses the flag, so every
+    other CTA must take its own copy after the 20 us wait -- the result may
+    not depend on CTA 0 being scheduled first."""
+    t = trace("c4")
+    with env(EBIC_DEBUG_MODE="4", **cfg):
+        with eb.Evaluator(t.matrix()) as ev:
+            for off, cols, counts, fit in t.batches[:3]:
+                f, c = ev.evaluate_population(eb.CbfPopulation(off, cols), eb.FitnessParams(t.sigma), t.eps,
+                                              return_counts=True)
+                assert (c == counts).all() and bits_equal(f, fit)
+
+
 def test_empty_population_and_errors():
     v = np.random.default_rng(1).standard_normal((100, 10))
     with eb.Evaluator(v) as ev:
