@@ -202,6 +202,7 @@ struct CountParams {
     uint32_t smem_window;
     uint32_t gap;         // K1v2: stage gaps of <= gap unreferenced columns (0-2)
     uint32_t compact;     // K1v2: stage the referenced columns (1) or whole tiles (0)
+    uint32_t prefetch;    // K1v2 compact: L2-prefetch the block this many items ahead (0 off)
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {

@@ -32,7 +32,6 @@
 
 namespace ebic_b200 {
 
-constexpr int kV2Producers = 4;     // producer warps (bulk-copy issue is per lane)
 constexpr int kV2MaxCols = 2048;    // bitmap of 64 words
 constexpr int kV2Chunk = 8;         // slots per warp iteration (4 groups x 2 series)
 constexpr int kV2MaxStages = 4;
@@ -49,14 +48,22 @@ struct V2Layout {
     uint32_t ucols;     // u16[n_cols] slot -> column
     uint32_t runs, run_slot;  // u32[max_runs] each
     uint32_t acc;       // u32[n_chunks][32] per-lane partial counts
+    uint32_t colw;      // u32[4][64] run-start / run-end word masks and prefix counts, u32[64] item tiles
     uint32_t excl;      // u64[kV2ExclItems] excl words of the CTA's items
     uint32_t area;      // first byte of the stage area (128-aligned)
 };
 
 __host__ __device__ inline uint32_t v2_max_runs(uint32_t n_cols) { return (n_cols + 1) / 2 + 1; }
 
-__host__ __device__ inline V2Layout v2_layout(uint32_t P, uint32_t L, uint32_t n_cols) {
+// Length buckets 2..12 are padded to whole chunks with dummy slots (so every
+// chunk of those lengths is uniform), bucket 1 so that bucket 2 starts on a
+// chunk: at most kV2Pad extra slots.
+constexpr uint32_t kV2Pad = 7 * 12;
+
+__host__ __device__ inline V2Layout v2_layout(uint32_t P0, uint32_t L0, uint32_t n_cols) {
     auto up16 = [](uint32_t x) { return (x + 15u) & ~15u; };
+    const uint32_t P = P0 + kV2Pad;        // slots, dummies included
+    const uint32_t L = L0 + kV2Pad * 12;  // list entries, dummies included
     V2Layout v;
     uint32_t at = 0;
     v.bars = at;     at += (2 * kMaxStages + 2) * 8;
@@ -75,6 +82,7 @@ __host__ __device__ inline V2Layout v2_layout(uint32_t P, uint32_t L, uint32_t n
     v.runs = at;     at = up16(at + 4 * v2_max_runs(n_cols));
     v.run_slot = at; at = up16(at + 4 * v2_max_runs(n_cols));
     v.acc = at;      at = up16(at + 4 * 32 * ((P + kV2Chunk - 1) / kV2Chunk));
+    v.colw = at;     at = up16(at + 4 * 4 * 64 + 4 * kV2ExclItems);  // + item tiles
     v.excl = at;     at = up16(at + 8 * kV2ExclItems);
     v.area = (at + 127u) & ~127u;
     return v;
@@ -84,20 +92,34 @@ __host__ __device__ inline V2Layout v2_layout(uint32_t P, uint32_t L, uint32_t n
 // stage area: rel u32[P+1], raw u16[L+16], wh u32[ceil(P/32)*64], hist,
 // hpad u32[64], wsum u32[32] -- the v1 builder's scratch.
 __host__ __device__ inline uint32_t v2_scratch_bytes(uint32_t P, uint32_t L) {
-    return static_cast<uint32_t>(count_scratch_bytes(P, L));
+    return static_cast<uint32_t>(count_scratch_bytes(P, L)) + 64 * 4;  // + original bucket counts
 }
 
 __device__ __forceinline__ uint32_t v2_slot_of(const uint32_t* bm, const uint32_t* bases, uint32_t c) {
     return bases[c >> 5] + __popc(bm[c >> 5] & ((1u << (c & 31)) - 1u));
 }
 
-// Producer warps: column bitmap, slots, runs (from the CBF).  All
-// kV2Producers warps load and mark; warp 0 then derives bases, ucols, runs.
+// Producer warps: column bitmap, slots, runs (from the CBF).  NP warps mark
+// the referenced columns; warp 0 turns the 64 bitmap words into slot bases
+// and run-start / run-end word masks with their prefix counts; then every
+// producer thread handles whole columns (slot -> column map, run starts and
+// ends by rank in their word) and finally whole runs.  Four barriers, no
+// serial per-bit loops.
+template <int NP>
 __device__ __forceinline__ void v2_build_columns(const CountParams& p, unsigned char* smem, const V2Layout& v,
                                                  int pw, int lane) {
     uint32_t* bm = reinterpret_cast<uint32_t*>(smem + v.bm);
+    uint32_t* bases = reinterpret_cast<uint32_t*>(smem + v.bases);
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + v.misc);
+    uint16_t* ucols = reinterpret_cast<uint16_t*>(smem + v.ucols);
+    uint32_t* runs = reinterpret_cast<uint32_t*>(smem + v.runs);
+    uint32_t* run_slot = reinterpret_cast<uint32_t*>(smem + v.run_slot);
+    uint32_t* smask = reinterpret_cast<uint32_t*>(smem + v.colw);  // run-start bits [64]
+    uint32_t* emask = smask + 64;                                  // run-end bits [64]
+    uint32_t* sbase = emask + 64;                                  // starts before word w [64]
+    uint32_t* ebase = sbase + 64;                                  // ends before word w [64]
     const int ptid = pw * 32 + lane;
-    constexpr int nthr = kV2Producers * 32;
+    constexpr int nthr = NP * 32;
     for (int w = ptid; w < 64; w += nthr) bm[w] = 0;
     named_bar_sync(2, nthr);
     const uint32_t L = p.total_len;
@@ -117,123 +139,100 @@ __device__ __forceinline__ void v2_build_columns(const CountParams& p, unsigned 
         for (int k = 0; k < kPer; ++k) {
             const uint32_t i = i0 + k * nthr;
             if (i >= n_vec) continue;
-            const uint32_t w4[4] = {x[k].x, x[k].y, x[k].z, x[k].w};
 #pragma unroll
             for (int h = 0; h < 8; ++h) {
                 const uint32_t pos = i * 8 + h;  // position from the aligned word
                 if (pos < shift || pos >= shift + L) continue;
-                const uint32_t c = (w4[h >> 1] >> (16 * (h & 1))) & 0xffffu;
+                const uint32_t wv = h < 2 ? x[k].x : h < 4 ? x[k].y : h < 6 ? x[k].z : x[k].w;
+                const uint32_t c = (wv >> (16 * (h & 1))) & 0xffffu;
                 atomicOr(&bm[c >> 5], 1u << (c & 31));
             }
         }
     }
     named_bar_sync(2, nthr);
-    if (pw != 0) return;
-    uint32_t* bases = reinterpret_cast<uint32_t*>(smem + v.bases);
-    uint16_t* ucols = reinterpret_cast<uint16_t*>(smem + v.ucols);
-    uint32_t* runs = reinterpret_cast<uint32_t*>(smem + v.runs);
-    uint32_t* run_slot = reinterpret_cast<uint32_t*>(smem + v.run_slot);
-    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + v.misc);
-    // word w = lane (low half) and lane + 32 (high half); column order =
-    // word order 0..63.  Gaps of <= p.gap unreferenced columns between two
-    // referenced ones are staged too (fewer, longer copies); the staged set
-    // replaces the bitmap, and slots follow it.
-    uint32_t x0 = bm[lane], x1 = bm[lane + 32];
-    if (p.gap) {
-        const uint32_t a0 = __shfl_up_sync(0xffffffffu, x0, 1), a1 = __shfl_up_sync(0xffffffffu, x1, 1);
-        const uint32_t n0 = __shfl_down_sync(0xffffffffu, x0, 1), n1 = __shfl_down_sync(0xffffffffu, x1, 1);
+    if (pw == 0) {
+        // word w = lane (low half) and lane + 32 (high half).  Gaps of <= p.gap
+        // unreferenced columns between referenced ones are staged too (fewer,
+        // longer copies); the staged set replaces the bitmap.
+        uint32_t x0 = bm[lane], x1 = bm[lane + 32];
         const uint32_t w31 = __shfl_sync(0xffffffffu, x0, 31), w32 = __shfl_sync(0xffffffffu, x1, 0);
-        const uint32_t pv0 = lane == 0 ? 0u : a0, pv1 = lane == 0 ? w31 : a1;
-        const uint32_t nx0 = lane == 31 ? w32 : n0, nx1 = lane == 31 ? 0u : n1;
-        auto fill = [&](uint32_t x, uint32_t prev, uint32_t next) {
-            const uint32_t m1 = (x << 1) | (prev >> 31), m2 = (x << 2) | (prev >> 30);
-            const uint32_t q1 = (x >> 1) | (next << 31), q2 = (x >> 2) | (next << 30);
-            uint32_t f = m1 & q1;                        // gap of one column
-            if (p.gap >= 2) f |= (m1 & q2) | (m2 & q1);  // gap of two
-            return x | f;
+        if (p.gap) {
+            const uint32_t a0 = __shfl_up_sync(0xffffffffu, x0, 1), a1 = __shfl_up_sync(0xffffffffu, x1, 1);
+            const uint32_t n0 = __shfl_down_sync(0xffffffffu, x0, 1), n1 = __shfl_down_sync(0xffffffffu, x1, 1);
+            const uint32_t pv0 = lane == 0 ? 0u : a0, pv1 = lane == 0 ? w31 : a1;
+            const uint32_t nx0 = lane == 31 ? w32 : n0, nx1 = lane == 31 ? 0u : n1;
+            auto fill = [&](uint32_t x, uint32_t prev, uint32_t next) {
+                const uint32_t m1 = (x << 1) | (prev >> 31), m2 = (x << 2) | (prev >> 30);
+                const uint32_t q1 = (x >> 1) | (next << 31), q2 = (x >> 2) | (next << 30);
+                uint32_t f = m1 & q1;                        // gap of one column
+                if (p.gap >= 2) f |= (m1 & q2) | (m2 & q1);  // gap of two
+                return x | f;
+            };
+            const uint32_t c0 = fill(x0, pv0, nx0), c1 = fill(x1, pv1, nx1);
+            x0 = c0;
+            x1 = c1;
+            bm[lane] = x0;
+            bm[lane + 32] = x1;
+        }
+        auto excl_scan = [&](uint32_t a, uint32_t& total) {
+            uint32_t incl = a;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            total = __shfl_sync(0xffffffffu, incl, 31);
+            return incl - a;
         };
-        const uint32_t c0 = fill(x0, pv0, nx0), c1 = fill(x1, pv1, nx1);
-        __syncwarp();
-        x0 = c0;
-        x1 = c1;
-        bm[lane] = x0;
-        bm[lane + 32] = x1;
-        __syncwarp();
-    }
-    auto excl_scan = [&](uint32_t a, uint32_t& total) {
-        uint32_t incl = a;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        total = __shfl_sync(0xffffffffu, incl, 31);
-        return incl - a;
-    };
-    uint32_t t0, t1;
-    const uint32_t b0 = excl_scan(__popc(x0), t0);
-    const uint32_t b1 = t0 + excl_scan(__popc(x1), t1);
-    bases[lane] = b0;
-    bases[lane + 32] = b1;
-    const uint32_t U = t0 + t1;
-    {
-        uint32_t x = x0, at = b0;
-        while (x) {
-            const int j = __ffs(x) - 1;
-            ucols[at++] = static_cast<uint16_t>(lane * 32 + j);
-            x &= x - 1;
-        }
-        x = x1;
-        at = b1;
-        while (x) {
-            const int j = __ffs(x) - 1;
-            ucols[at++] = static_cast<uint16_t>((lane + 32) * 32 + j);
-            x &= x - 1;
+        // neighbouring bits for run starts (previous column clear) and ends
+        // (next column clear)
+        const uint32_t g31 = __shfl_sync(0xffffffffu, x0, 31), g32 = __shfl_sync(0xffffffffu, x1, 0);
+        const uint32_t up0 = __shfl_up_sync(0xffffffffu, x0 >> 31, 1), up1 = __shfl_up_sync(0xffffffffu, x1 >> 31, 1);
+        const uint32_t dn0 = __shfl_down_sync(0xffffffffu, x0 & 1u, 1), dn1 = __shfl_down_sync(0xffffffffu, x1 & 1u, 1);
+        const uint32_t pt0 = lane == 0 ? 0u : up0, pt1 = lane == 0 ? (g31 >> 31) : up1;
+        const uint32_t nb0 = lane == 31 ? (g32 & 1u) : dn0, nb1 = lane == 31 ? 0u : dn1;
+        const uint32_t s0 = x0 & ~((x0 << 1) | pt0), s1 = x1 & ~((x1 << 1) | pt1);
+        const uint32_t e0 = x0 & ~((x0 >> 1) | (nb0 << 31)), e1 = x1 & ~((x1 >> 1) | (nb1 << 31));
+        uint32_t t0, t1, ts0, ts1, te0, te1;
+        const uint32_t b0 = excl_scan(__popc(x0), t0);
+        const uint32_t b1 = t0 + excl_scan(__popc(x1), t1);
+        const uint32_t rs0 = excl_scan(__popc(s0), ts0);
+        const uint32_t rs1 = ts0 + excl_scan(__popc(s1), ts1);
+        const uint32_t re0 = excl_scan(__popc(e0), te0);
+        const uint32_t re1 = te0 + excl_scan(__popc(e1), te1);
+        bases[lane] = b0;
+        bases[lane + 32] = b1;
+        smask[lane] = s0;
+        smask[lane + 32] = s1;
+        emask[lane] = e0;
+        emask[lane + 32] = e1;
+        sbase[lane] = rs0;
+        sbase[lane + 32] = rs1;
+        ebase[lane] = re0;
+        ebase[lane + 32] = re1;
+        if (lane == 0) {
+            misc[0] = t0 + t1;    // U
+            misc[1] = ts0 + ts1;  // runs
         }
     }
-    // runs: start bit = set with the previous column clear; end bit = set
-    // with the next column clear (bits of the neighbouring words via shuffles)
-    const uint32_t prev_top0 = __shfl_up_sync(0xffffffffu, x0 >> 31, 1);
-    const uint32_t x0_last = __shfl_sync(0xffffffffu, x0, 31);
-    const uint32_t prev_top1_raw = __shfl_up_sync(0xffffffffu, x1 >> 31, 1);
-    const uint32_t pt0 = lane == 0 ? 0u : prev_top0;
-    const uint32_t pt1 = lane == 0 ? (x0_last >> 31) : prev_top1_raw;
-    const uint32_t next_bot0_raw = __shfl_down_sync(0xffffffffu, x0 & 1u, 1);
-    const uint32_t x1_first = __shfl_sync(0xffffffffu, x1, 0);
-    const uint32_t next_bot1_raw = __shfl_down_sync(0xffffffffu, x1 & 1u, 1);
-    const uint32_t nb0 = lane == 31 ? (x1_first & 1u) : next_bot0_raw;
-    const uint32_t nb1 = lane == 31 ? 0u : next_bot1_raw;
-    const uint32_t s0 = x0 & ~((x0 << 1) | pt0), s1 = x1 & ~((x1 << 1) | pt1);
-    const uint32_t e0 = x0 & ~((x0 >> 1) | (nb0 << 31)), e1 = x1 & ~((x1 >> 1) | (nb1 << 31));
-    uint32_t ts0, ts1, te0, te1;
-    const uint32_t rs0 = excl_scan(__popc(s0), ts0);
-    const uint32_t rs1 = ts0 + excl_scan(__popc(s1), ts1);
-    const uint32_t re0 = excl_scan(__popc(e0), te0);
-    const uint32_t re1 = te0 + excl_scan(__popc(e1), te1);
-    const uint32_t n_runs = ts0 + ts1;
-    // starts into runs[] (column), ends into run_slot[] temporarily
-    auto put = [&](uint32_t x, uint32_t at, uint32_t word, uint32_t* out) {
-        while (x) {
-            const int j = __ffs(x) - 1;
-            out[at++] = word * 32 + j;
-            x &= x - 1;
-        }
-    };
-    put(s0, rs0, lane, runs);
-    put(s1, rs1, lane + 32, runs);
-    put(e0, re0, lane, run_slot);
-    put(e1, re1, lane + 32, run_slot);
-    __syncwarp();
-    for (uint32_t r = lane; r < n_runs; r += 32) {
+    named_bar_sync(2, nthr);
+    // column-parallel: slot -> column map; run starts (into runs[]) and ends
+    // (into run_slot[], temporarily), each at its rank
+    for (uint32_t c = ptid; c < p.n_cols; c += nthr) {
+        const uint32_t w = c >> 5, lt = (1u << (c & 31)) - 1u, bit = 1u << (c & 31);
+        const uint32_t x = bm[w];
+        if (x & bit) ucols[bases[w] + __popc(x & lt)] = static_cast<uint16_t>(c);
+        const uint32_t sm = smask[w], em = emask[w];
+        if (sm & bit) runs[sbase[w] + __popc(sm & lt)] = c;
+        if (em & bit) run_slot[ebase[w] + __popc(em & lt)] = c;
+    }
+    named_bar_sync(2, nthr);
+    const uint32_t n_runs = misc[1];
+    for (uint32_t r = ptid; r < n_runs; r += nthr) {
         const uint32_t c0 = runs[r], c1 = run_slot[r];
         runs[r] = (c0 << 16) | (c1 - c0 + 1);
         run_slot[r] = v2_slot_of(bm, bases, c0);
     }
-    __syncwarp();
-    if (lane == 0) {
-        misc[0] = U;
-        misc[1] = n_runs;
-    }
-    __syncwarp();
+    named_bar_sync(2, nthr);
 }
 
 // Consumer-side work list (NCW warps): the v1 counting sort by length
@@ -242,8 +241,16 @@ __device__ __forceinline__ void v2_build_columns(const CountParams& p, unsigned 
 template <int CHUNK>
 __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigned char* smem, const V2Layout& v,
                                                    const WorkList& w, uint64_t* cols_ready, int tid, int nthreads,
-                                                   int bar_id) {
+                                                   int bar_id, const uint32_t* item_tile, uint32_t n_my_items,
+                                                   uint32_t rows_per_tile) {
     const uint32_t P = p.n_series, L = p.total_len;
+    // excl words of this CTA's items (rows the layout cannot represent): the
+    // loads ride along with the CBF's, no extra round trip before the walk
+    unsigned long long* excl_items = reinterpret_cast<unsigned long long*>(smem + v.excl);
+    if (p.row_excl && tid < kV2ExclItems) {
+        const unsigned long long x = tid < n_my_items ? __ldg(p.row_excl + ((item_tile[tid] * rows_per_tile) >> 6)) : 0ull;
+        excl_items[tid] = x;
+    }
     const uint32_t nblk = (P + 31) / 32;
     const int lane = tid & 31, nw = nthreads >> 5;
     const uint64_t base = p.cols_base;
@@ -270,10 +277,10 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
     }
     for (uint32_t i = tid; i < nblk * kLenBuckets; i += nthreads) w.wh[i] = 0;
     for (int b = tid; b < kLenBuckets; b += nthreads) w.hist[b] = 0;
-    for (uint32_t i = tid; i < P + 2; i += nthreads) w.cnt[i] = 0;
+    for (uint32_t i = tid; i < P + kV2Pad + 2; i += nthreads) w.cnt[i] = 0;
     {
         uint32_t* acc = reinterpret_cast<uint32_t*>(smem + v.acc);
-        const uint32_t n_acc = 32u * ((P + CHUNK - 1) / CHUNK);
+        const uint32_t n_acc = 32u * ((P + kV2Pad + CHUNK - 1) / CHUNK);
         for (uint32_t i = tid; i < n_acc; i += nthreads) acc[i] = 0;
     }
     named_bar_sync(bar_id, nthreads);  // 1
@@ -293,10 +300,17 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
     }
     named_bar_sync(bar_id, nthreads);  // 2
 
+    uint32_t* orig = w.wsum + 32;  // original bucket counts
     if (tid < 32) {
+        for (int k = 0; k < 2; ++k) orig[tid + 32 * k] = w.hist[tid + 32 * k];
+        __syncwarp();
         for (int k = 0; k < 2; ++k) {
             const int b = tid + 32 * k;
-            w.hpad[b] = b < kLenBuckets - 1 ? w.hist[b] * pad4(b) : 0u;
+            uint32_t c = orig[b];
+            if (b >= 2 && b <= 12) c = (c + CHUNK - 1) / CHUNK * CHUNK;
+            if (b == 1) c = (orig[0] + orig[1] + CHUNK - 1) / CHUNK * CHUNK - orig[0];
+            w.hist[b] = c;
+            w.hpad[b] = b < kLenBuckets - 1 ? c * pad4(b) : 0u;
         }
         __syncwarp();
         warp_scan64(w.hist, w.hpad, tid);
@@ -344,19 +358,38 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
                 w.pcols[st + i] = i < len ? slot_of(from[i]) * 128u : 0u;
         }
     }
+    // dummy slots of the padded buckets 1..12: no series (sl = ~0), a zero
+    // offset list (slot 0's column); their counts are never read
+    const uint32_t pslots = w.hist[kLenBuckets - 1] + orig[kLenBuckets - 1];  // slots incl. dummies
+    for (uint32_t t = tid; t < 12 * CHUNK; t += nthreads) {
+        const uint32_t b = 1 + t / CHUNK, j = t % CHUNK;
+        const uint32_t bucket_slots = w.hist[b + 1] - w.hist[b];
+        if (orig[b] + j >= bucket_slots) continue;
+        const uint32_t r = orig[b] + j;
+        const uint32_t g = w.hist[b] + r;
+        const uint32_t st = w.hpad[b] + r * pad4(b);
+        w.sl[g] = 0xffffffffu;
+        w.slen[g] = b;
+        w.sstart[g] = st;
+        for (uint32_t i = 0; i < pad4(b); ++i) w.pcols[st + i] = 0u;
+        if (g % CHUNK == 0)
+            reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = (b >= 2 && b <= 12) ? ((st << 8) | b) : 0u;
+    }
+    if (tid == 0) reinterpret_cast<uint32_t*>(smem + v.misc)[3] = pslots;
     named_bar_sync(bar_id, nthreads);  // 4
 
     const uint32_t ovf = w.hist[kLenBuckets - 1];
-    if (ovf < P) {
+    const uint32_t P_slots = pslots;
+    if (ovf < P_slots) {
         if (tid == 0) {
             uint32_t run = w.hpad[kLenBuckets - 1];
-            for (uint32_t g = ovf; g < P; ++g) {
+            for (uint32_t g = ovf; g < P_slots; ++g) {
                 w.sstart[g] = run;
                 run += pad4(w.slen[g]);
             }
         }
         named_bar_sync(bar_id, nthreads);
-        for (uint32_t g = ovf + tid; g < P; g += nthreads) {
+        for (uint32_t g = ovf + tid; g < P_slots; g += nthreads) {
             const uint32_t len = w.slen[g], st = w.sstart[g];
             const uint16_t* from = w.raw + w.rel[w.sl[g]];
             for (uint32_t i = 0; i < pad4(len); ++i)
@@ -365,7 +398,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
     }
     // overflow-bucket chunks (lengths >= 63) take the per-slot path
     uint32_t* cdesc = reinterpret_cast<uint32_t*>(smem + v.cdesc);
-    for (uint32_t ch = (ovf + CHUNK - 1) / CHUNK + tid; ch < (P + CHUNK - 1) / CHUNK; ch += nthreads) cdesc[ch] = 0u;
+    for (uint32_t ch = (ovf + CHUNK - 1) / CHUNK + tid; ch < (P_slots + CHUNK - 1) / CHUNK; ch += nthreads) cdesc[ch] = 0u;
     if (ovf % CHUNK && tid == 0) cdesc[ovf / CHUNK] = 0u;
     named_bar_sync(bar_id, nthreads);  // 5
 }
@@ -421,12 +454,12 @@ __device__ __forceinline__ uint32_t v2_count_uniform(uint32_t L, uint32_t base, 
 
 // ---------------------------------------------------------------------------
 // K1v2.  PLANES: 1 (64-row tiles) or 2 (32-row tiles); 128-byte slices.
-// Grid: persistent, <= SMs; block: (NCW + kV2Producers) warps.
+// Grid: persistent, <= SMs; block: NCW consumer + NP producer warps.
 // p.compact: stage the launch's referenced columns (runs); else whole tiles,
 // one contiguous bulk copy each (short launches: no wait for the column set).
 // ---------------------------------------------------------------------------
-template <int PLANES, int NCW>
-__global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
+template <int PLANES, int NCW, int NP>
+__global__ void __launch_bounds__((NCW + NP) * 32, 1)
     count_v2_kernel(const CountParams p) {
     using W = RankWalker<PLANES, 128, 2>;
     constexpr int RPG = W::kRowsPerTile;  // 64 or 32
@@ -543,8 +576,8 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
         } else {
             // the host CBF is in device memory once this CTA's consumers are
             // past stage_host_cbf (barrier 3: consumers + producers)
-            if (p.host_cbf) named_bar_sync(3, (NCW + kV2Producers) * 32);
-            v2_build_columns(p, smem, v, pw, lane);
+            if (p.host_cbf) named_bar_sync(3, (NCW + NP) * 32);
+            v2_build_columns<NP>(p, smem, v, pw, lane);
             if (pw == 0 && lane == 0) {
                 const uint32_t sb = misc[0] * 128u;
                 uint32_t n = sb ? min(static_cast<uint32_t>(kV2MaxStages), area_bytes / sb) : 1u;
@@ -567,24 +600,44 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
             if (p.debug_mode != 3) {
                 for (uint32_t item = blockIdx.x; item < n_items; item += G, ++issued) {
                     const uint32_t tile = item < full ? item : full + (item - full) / parts;
+                    unsigned long long* is = (p.phase_ns && blockIdx.x == 0 && issued < 64)
+                                                 ? p.phase_ns + 8ull * (512 + issued) : nullptr;
                     if (ptid == 0) {  // one thread waits; the others sleep in the named barrier
+                        if (is) is[0] = global_ns();
                         if (issued < stages && (st + 1) * stage_bytes > scratch_at) mbar_wait(prol_bar, 0);
                         mbar_wait(&empty_bar[st], phase ^ 1u);
-                        if (p.debug_mode == 2) mbar_arrive(&full_bar[st]);
+                        if (is) is[1] = global_ns();
+                            if (p.debug_mode == 2) mbar_arrive(&full_bar[st]);
                         else mbar_arrive_expect_tx(&full_bar[st], stage_bytes);
                     }
-                    named_bar_sync(2, kV2Producers * 32);
+                    named_bar_sync(2, NP * 32);
                     if (p.debug_mode != 2) {
                         const uint32_t dst = area_addr + st * stage_bytes;
                         const uint32_t bar = full_addr0 + st * 8u;
                         const unsigned char* srcb = ranks + size_t(tile) * block_bytes;
-                        for (uint32_t r = ptid; r < n_runs; r += kV2Producers * 32) {
+                        for (uint32_t r = ptid; r < n_runs; r += NP * 32) {
                             const uint32_t x = runs[r];
                             asm volatile(
                                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                                     dst + run_slot[r] * 128u),
                                 "l"(srcb + size_t(x >> 16) * 128u), "r"((x & 0xffffu) * 128u), "r"(bar)
                                 : "memory");
+                        }
+                        if (is && ptid == 0) is[2] = global_ns();
+                        // Keep HBM busy beyond the ring: warm L2 with the
+                        // block of the tile p.prefetch items ahead, so its
+                        // copies into shared memory later come from L2.
+                        if (p.prefetch && ptid == 32) {
+                            const uint32_t ahead = item + p.prefetch * G;
+                            if (ahead < n_items) {
+                                const uint32_t ta = ahead < full ? ahead : full + (ahead - full) / parts;
+                                const unsigned char* pb = ranks + size_t(ta) * block_bytes;
+                                for (uint32_t o = 0; o < block_bytes; o += 65536u) {
+                                    const uint32_t n = static_cast<uint32_t>(block_bytes - o < 65536u ? block_bytes - o : 65536u);
+                                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pb + o), "r"(n)
+                                                 : "memory");
+                                }
+                            }
                         }
                     }
                     if (++st == stages) st = 0, phase ^= 1u;
@@ -597,19 +650,33 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
             stage_host_cbf(p, threadIdx.x, NCW * 32, 1);
             if (compact) {
                 __threadfence_block();
-                named_bar_sync(3, (NCW + kV2Producers) * 32);  // releases the producers (column set)
+                named_bar_sync(3, (NCW + NP) * 32);  // releases the producers (column set)
             }
         }
-        v2_build_work_list<CHUNK>(p, smem, v, wl, compact ? cols_ready : nullptr, threadIdx.x, NCW * 32, 1);
+        {
+            // tiles of this CTA's first kV2ExclItems items (for the excl preload)
+            uint32_t* item_tile = reinterpret_cast<uint32_t*>(smem + v.colw) + 256;
+            uint32_t n_my = 0;
+            for (uint32_t item = blockIdx.x; item < n_items && n_my < kV2ExclItems; item += G) ++n_my;
+            if (threadIdx.x < n_my) {
+                const uint32_t item = blockIdx.x + threadIdx.x * G;
+                item_tile[threadIdx.x] = item < full ? item : full + (item - full) / parts;
+            }
+            named_bar_sync(1, NCW * 32);
+            v2_build_work_list<CHUNK>(p, smem, v, wl, compact ? cols_ready : nullptr, threadIdx.x, NCW * 32, 1,
+                                      item_tile, n_my, RPG);
+        }
         if (threadIdx.x == 0) mbar_arrive(prol_bar);
         if (stamp && threadIdx.x == 0) stamp[1] = global_ns();
         const uint32_t stages = compact ? misc[2] : p.stages;
         const uint32_t stage_bytes = compact ? misc[0] * 128u : p.n_cols * 128u;
+        const uint32_t P_slots = misc[3];  // slots incl. the padded buckets' dummies
+        const uint32_t n_chunks_s = (P_slots + CHUNK - 1) / CHUNK;
 
         // rows the collapsed layout cannot represent, evaluated in fp64 (see v1)
         for (uint32_t i = G - 1 - blockIdx.x; i < p.n_excl; i += G) {
             const double* rowv = p.excl_vals + size_t(i) * p.n_cols;
-            for (uint32_t g = threadIdx.x; g < P; g += NCW * 32) {
+            for (uint32_t g = threadIdx.x; g < P_slots; g += NCW * 32) {
                 const uint32_t len = wl.slen[g];
                 const uint32_t* pc = wl.pcols + wl.sstart[g];
                 auto col = [&](uint32_t off) -> uint32_t { return compact ? ucols[off >> 7] : (off >> 7); };
@@ -634,27 +701,15 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
         // excl words of this CTA's first kV2ExclItems items (rows the layout
         // cannot represent), loaded once instead of a dependent global load
         // per item right before its walk
-        unsigned long long* excl_items = reinterpret_cast<unsigned long long*>(smem + v.excl);
-        if (p.row_excl) {
-            for (uint32_t t = threadIdx.x; t < kV2ExclItems; t += NCW * 32) {
-                const uint32_t item = blockIdx.x + t * G;
-                unsigned long long w = 0ull;
-                if (item < n_items) {
-                    const uint32_t tl = item < full ? item : full + (item - full) / parts;
-                    w = __ldg(p.row_excl + ((tl * RPG) >> 6));
-                }
-                excl_items[t] = w;
-            }
-            named_bar_sync(1, NCW * 32);
-        }
+        const unsigned long long* excl_items = reinterpret_cast<const unsigned long long*>(smem + v.excl);
         uint32_t it = 0;  // this CTA's item number
         for (uint32_t item = blockIdx.x; item < n_items; item += G, ++it) {
-            uint32_t tile = item, c_lo = 0, c_hi = n_chunks;
+            uint32_t tile = item, c_lo = 0, c_hi = n_chunks_s;
             if (item >= full) {  // a part of a last-wave tile: a chunk range
                 const uint32_t j = item - full, part = j % parts;
                 tile = full + j / parts;
-                c_lo = part * n_chunks / parts;
-                c_hi = (part + 1) * n_chunks / parts;
+                c_lo = part * n_chunks_s / parts;
+                c_hi = (part + 1) * n_chunks_s / parts;
             }
             const uint32_t r0 = tile * RPG + gl * RPL;
             uint32_t excl = 0;
@@ -687,7 +742,7 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
                         c = 0;
 #pragma unroll
                         for (int q = 0; q < SPG; ++q)
-                            if (g0 + q < P)
+                            if (g0 + q < P_slots)
                                 c |= W::count_any(base, wl.pcols + wl.sstart[g0 + q], wl.slen[g0 + q], vm) << (16 * q);
                     }
                     if (c) atomicAdd(&acc[ch * 32 + lane], c);
@@ -709,14 +764,18 @@ __global__ void __launch_bounds__((NCW + kV2Producers) * 32, 1)
         const int grp = lane / GL, gl = lane % GL;
         for (uint32_t i = threadIdx.x; i < ((P + 3u) & ~3u); i += blockDim.x) by_series[i] = 0;
         __syncthreads();
-        for (uint32_t ch = warp; ch < n_chunks; ch += nwarps) {
+        const uint32_t P_slots = misc[3];
+        for (uint32_t ch = warp; ch < (P_slots + CHUNK - 1) / CHUNK; ch += nwarps) {
             uint32_t x = acc[ch * 32 + lane];
 #pragma unroll
             for (int o = GL / 2; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
             const uint32_t g0 = ch * CHUNK + grp * SPG;
             if (gl == 0) {
-                if (g0 < P) by_series[wl.sl[g0]] = wl.cnt[g0] + (x & 0xffffu);
-                if (g0 + 1 < P) by_series[wl.sl[g0 + 1]] = wl.cnt[g0 + 1] + (x >> 16);
+#pragma unroll
+                for (int q = 0; q < SPG; ++q) {
+                    const uint32_t s = g0 + q < P_slots ? wl.sl[g0 + q] : 0xffffffffu;
+                    if (s != 0xffffffffu) by_series[s] = wl.cnt[g0 + q] + ((x >> (16 * q)) & 0xffffu);
+                }
             }
         }
         __syncthreads();

@@ -1,0 +1,42 @@
+"""Per-item timeline of CTA 0 in K1v2 (EBIC_PHASE_TIMING=1, device path):
+producer wait-for-free-stage / issue-done, consumer warp 0 wait-for-data /
+walk-done, for one workload.  usage: python tools/probes/item_stamps.py [c5ss]"""
+import ctypes as C
+import os
+import sys
+from pathlib import Path
+import numpy as np
+os.environ["EBIC_PHASE_TIMING"] = "1"
+ROOT = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(ROOT)); sys.path.insert(0, str(ROOT / "tests"))
+import torch  # noqa: E402
+import paper_1801_03039_b200 as eb  # noqa: E402
+from paper_1801_03039_b200 import _lib  # noqa: E402
+from golden_io import trace  # noqa: E402
+
+t = trace(sys.argv[1] if len(sys.argv) > 1 else "c5ss")
+off, cols, _, _ = t.batches[-1]
+with eb.Evaluator(t.matrix()) as ev:
+    d_off = torch.from_numpy(off.astype(np.int64)).cuda()
+    d_cols = torch.from_numpy(cols.view(np.int16)).cuda()
+    P, L = len(off) - 1, int(off[-1])
+    cnt = torch.zeros(P, dtype=torch.int64, device="cuda")
+    fit = torch.zeros(P, dtype=torch.float64, device="cuda")
+    for _ in range(4):
+        _lib.check(_lib.lib.ebic_count_matches_device(ev.handle, d_off.data_ptr(), d_cols.data_ptr(), P, L,
+                                                      t.eps, t.sigma, cnt.data_ptr(), fit.data_ptr(), None))
+        torch.cuda.synchronize()
+    st = np.zeros((4096, 8), dtype=np.uint64)
+    n = C.c_size_t(0)
+    _lib.check(_lib.lib.ebic_ctx_phase_times(ev.handle, st.ctypes.data_as(_lib.u64p), 4096, C.byref(n)))
+    st = st.astype(np.int64)
+    t0 = st[:n.value, 0].min()
+    it = st[512:576]
+    print("CTA0 prologue end", (st[0, 1] - t0) / 1e3, "walk end", (st[0, 2] - t0) / 1e3, "kernel end", (st[:n.value, 3].max() - t0) / 1e3)
+    print("item  prod_start  stage_free  issued   cons_wait  data_in  walk_done   (us from first CTA start)")
+    for k in range(64):
+        r = it[k]
+        if r[3] == 0 and r[0] == 0:
+            continue
+        f = lambda x: f"{(x - t0) / 1e3:9.2f}" if x else "        -"  # noqa: E731
+        print(f"{k:4d} {f(r[0])} {f(r[1])} {f(r[2])} {f(r[3])} {f(r[4])} {f(r[5])}")
