@@ -32,6 +32,9 @@ with eb.Evaluator(t.matrix()) as ev:
     st = st.astype(np.int64)
     t0 = st[:n.value, 0].min()
     it = st[512:576]
+    pr = st[600]
+    print("CTA0 prologue: start->item tiles", (pr[0] - st[0, 0]) / 1e3, "barriers 1..5 at",
+          [round((pr[k] - st[0, 0]) / 1e3, 2) for k in range(1, 6)], "(us from CTA 0 start)")
     print("CTA0 prologue end", (st[0, 1] - t0) / 1e3, "walk end", (st[0, 2] - t0) / 1e3, "kernel end", (st[:n.value, 3].max() - t0) / 1e3)
     print("item  prod_start  stage_free  issued   cons_wait  data_in  walk_done   (us from first CTA start)")
     for k in range(64):
