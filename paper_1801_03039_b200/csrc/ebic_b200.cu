@@ -1037,6 +1037,8 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             flag.store((int)smem, std::memory_order_release);
         }
+        s.last_cfg.ncw = ncw;                     // reported by ebic_ctx_get_info
+        s.last_cfg.stages = compact ? 0 : (int)p.stages;  // compacted: chosen in-kernel from U
         void* args[1] = {const_cast<CountParams*>(&p)};
         launch_kernel(&s, fn, grid, (ncw + np) * 32, smem, st, args);
         CK(cudaGetLastError());

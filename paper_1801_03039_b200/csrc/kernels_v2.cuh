@@ -369,6 +369,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
             for (uint32_t q = 0; q < pad4(len) / 4; ++q) owner[st / 4 + q] = static_cast<uint16_t>(g);
         }
     }
+    if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 601] = global_ns();
     // dummy slots of the padded buckets 1..12: no series (sl = ~0), a zero
     // offset list (slot 0's column); their counts are never read
     const uint32_t pslots = w.hist[kLenBuckets - 1] + orig[kLenBuckets - 1];  // slots incl. dummies
@@ -387,7 +388,9 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
             reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = (b >= 2 && b <= 12) ? ((st << 8) | b) : 0u;
     }
     if (tid == 0) reinterpret_cast<uint32_t*>(smem + v.misc)[3] = pslots;
+    if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 601 + 1] = global_ns();
     named_bar_sync(bar_id, nthreads);  // 4a
+    if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 601 + 2] = global_ns();
     // The lists of buckets < 63, four entries per thread: slot byte offsets
     // of the series' columns, zero past its length (and for dummies).  A
     // series-per-thread fill would leave the longest series on the critical

@@ -35,6 +35,9 @@ with eb.Evaluator(t.matrix()) as ev:
     pr = st[600]
     print("CTA0 prologue: start->item tiles", (pr[0] - st[0, 0]) / 1e3, "barriers 1..5 at",
           [round((pr[k] - st[0, 0]) / 1e3, 2) for k in range(1, 6)], "(us from CTA 0 start)")
+    pd = st[601]
+    print("  phase D (thread 0): slots done", (pd[0] - st[0, 0]) / 1e3, "dummies done", (pd[1] - st[0, 0]) / 1e3,
+          "after barrier 4a", (pd[2] - st[0, 0]) / 1e3)
     print("CTA0 prologue end", (st[0, 1] - t0) / 1e3, "walk end", (st[0, 2] - t0) / 1e3, "kernel end", (st[:n.value, 3].max() - t0) / 1e3)
     print("item  prod_start  stage_free  issued   cons_wait  data_in  walk_done   (us from first CTA start)")
     for k in range(64):
