@@ -303,7 +303,7 @@ void grow_pinned(unsigned char** p, size_t* cap, size_t need) {
 // mode: 0 tree, 1 u32 stripes [P][8], 2 fp32 stripes [8][P rounded to 4] (K1v2)
 void ensure_partial(Shard& s, size_t P, int grid, int mode) {
     const size_t gsz = reduce_group_size((uint32_t)grid);
-    const size_t need = mode == 2 ? ((P + 3) & ~size_t(3)) * kStripes
+    const size_t need = mode == 2 ? ((P + kV2Pad + 7) & ~size_t(7)) * kStripes  // slots incl. dummies, whole chunks
                         : mode == 1 ? P * kStripes : (size_t(grid) + (grid + gsz - 1) / gsz) * P;
     if (need <= s.partial_cap && mode == s.last_reduce) return;
     // a launch still queued on the previous stream may use the old scratch

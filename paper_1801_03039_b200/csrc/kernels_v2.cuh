@@ -491,6 +491,71 @@ __device__ __forceinline__ uint32_t v2_count_uniform(uint32_t L, uint32_t base, 
     }
 }
 
+// Cross-CTA tail in slot order (see the kernel).  Stripes [kStripes][PS4]
+// fp32, PS4 = the slot count rounded to a whole chunk (the host sizes them for P + kV2Pad
+// slots); integer counts below 2^24 are exact in fp32.
+template <int GL, int SPG, uint32_t CHUNK>
+__device__ __forceinline__ void v2_tail_slots(const CountParams& p, const WorkList& wl, const uint32_t* acc,
+                                              uint32_t P_slots, int warp, int lane) {
+    static_assert(GL == 8 && SPG == 2 && CHUNK == 8, "chunk = 4 groups x 2 slots");
+    const uint32_t PS4 = (p.n_series + kV2Pad + 7u) & ~7u;  // whole chunks
+    float* stripes = reinterpret_cast<float*>(p.partial);
+    const uint32_t stripe = blockIdx.x % kStripes;
+    unsigned long long* stamp = p.phase_ns ? p.phase_ns + 8ull * blockIdx.x : nullptr;
+    const int nwarps = blockDim.x >> 5;
+    const uint32_t n_chunks = (P_slots + CHUNK - 1) / CHUNK;
+    for (uint32_t ch = warp; ch < n_chunks; ch += nwarps) {
+        uint32_t x = acc[ch * 32 + lane];
+#pragma unroll
+        for (int o = GL / 2; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        // lane 8k holds slots 2k, 2k+1 of the chunk; gather 4 slots per lane
+        // 0 (slots 0-3) and lane 16 (slots 4-7)
+        const uint32_t g = ch * CHUNK + (lane / GL) * SPG;
+        const uint32_t c0 = (x & 0xffffu) + (g < P_slots ? wl.cnt[g] : 0u);
+        const uint32_t c1 = (x >> 16) + (g + 1 < P_slots ? wl.cnt[g + 1] : 0u);
+        const uint32_t n0 = __shfl_down_sync(0xffffffffu, c0, GL), n1 = __shfl_down_sync(0xffffffffu, c1, GL);
+        if ((lane & (2 * GL - 1)) == 0 && (c0 | c1 | n0 | n1))
+            asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
+                             stripes + size_t(stripe) * PS4 + ch * CHUNK + (lane / GL) * SPG),
+                         "f"(static_cast<float>(c0)), "f"(static_cast<float>(c1)), "f"(static_cast<float>(n0)),
+                         "f"(static_cast<float>(n1))
+                         : "memory");
+    }
+    __shared__ int s_last;
+    __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[4] = global_ns();
+    if (threadIdx.x == 0) s_last = ticket_acq_rel(&p.done[kMaxGroups]) == gridDim.x - 1;
+    __syncthreads();
+    if (stamp && threadIdx.x == 0) stamp[5] = global_ns();
+    if (!s_last) return;
+    if (stamp && threadIdx.x == 0) stamp[7] = global_ns();
+    for (uint32_t g = threadIdx.x; g < P_slots; g += blockDim.x) {
+        float v[kStripes];
+#pragma unroll
+        for (int k = 0; k < kStripes; ++k) v[k] = __ldcg(stripes + size_t(k) * PS4 + g);
+        double t = 0.0;
+#pragma unroll
+        for (int k = 0; k < kStripes; ++k) t += static_cast<double>(v[k]);
+#pragma unroll
+        for (int k = 0; k < kStripes; ++k) __stcg(stripes + size_t(k) * PS4 + g, 0.0f);
+        const uint32_t s = wl.sl[g];
+        if (s == 0xffffffffu) continue;  // dummy slot
+        const uint64_t c = static_cast<uint64_t>(t);
+        if (p.xacc) {
+            if (c) atomicAdd_system(p.xacc + s, static_cast<unsigned long long>(c));
+            continue;
+        }
+        p.counts_out[s] = c;
+        if (p.fitness_out) p.fitness_out[s] = fitness_from_tables(c, wl.slen[g], p.sigma, p.logt, p.expt);
+    }
+    if (threadIdx.x == 0) p.done[kMaxGroups] = 0u;
+    if (p.xacc) {
+        cross_shard_finish(p);
+        return;
+    }
+    signal_done(p);
+}
+
 // ---------------------------------------------------------------------------
 // K1v2.  PLANES: 1 (64-row tiles) or 2 (32-row tiles); 128-byte slices.
 // Grid: persistent, <= SMs; block: NCW consumer + NP producer warps.
@@ -792,11 +857,18 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
     }
     __syncthreads();
     if (stamp && threadIdx.x == 0) stamp[2] = global_ns();
-    // Sum each chunk's per-lane words over its groups' lanes, add the fp64
-    // fix-up rows, and store the CTA's counts by series (the stage area is
-    // idle now) for the cross-CTA tail.
-    uint32_t* by_series = reinterpret_cast<uint32_t*>(area);
-    {
+    if (p.reduce_striped == 2) {
+        // Slot-order tail: every CTA builds the same slot order, so the
+        // stripes are indexed by slot ([8][whole chunks] fp32) and a
+        // chunk's 8 slot counts go out as two 4-wide reductions straight
+        // from the lane sums -- no series-order scatter; the last CTA maps
+        // slots to series.
+        v2_tail_slots<GL, SPG, CHUNK>(p, wl, acc, misc[3], warp, lane);
+    } else {
+        // Sum each chunk's per-lane words over its groups' lanes, add the fp64
+        // fix-up rows, and store the CTA's counts by series (the stage area
+        // is idle now) for the cross-CTA tail.
+        uint32_t* by_series = reinterpret_cast<uint32_t*>(area);
         const int nwarps = blockDim.x >> 5;
         const int grp = lane / GL, gl = lane % GL;
         for (uint32_t i = threadIdx.x; i < ((P + 3u) & ~3u); i += blockDim.x) by_series[i] = 0;
@@ -816,9 +888,8 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
             }
         }
         __syncthreads();
+        count_epilogue(p, by_series, nullptr);
     }
-    if (p.reduce_striped == 2) count_epilogue_v4(p, by_series);
-    else count_epilogue(p, by_series, nullptr);
     if (stamp && threadIdx.x == 0) stamp[3] = global_ns();
 }
 

@@ -39,6 +39,13 @@ with eb.Evaluator(t.matrix()) as ev:
     print("  phase D (thread 0): slots done", (pd[0] - st[0, 0]) / 1e3, "dummies done", (pd[1] - st[0, 0]) / 1e3,
           "after barrier 4a", (pd[2] - st[0, 0]) / 1e3)
     print("CTA0 prologue end", (st[0, 1] - t0) / 1e3, "walk end", (st[0, 2] - t0) / 1e3, "kernel end", (st[:n.value, 3].max() - t0) / 1e3)
+    a = st[:n.value]
+    q = lambda col: np.percentile((a[:, col] - t0) / 1e3, [0, 50, 100]).round(2).tolist()  # noqa: E731
+    print("all CTAs (min/median/max us): start", q(0), "prologue end", q(1), "walk end", q(2),
+          "reds done", q(4), "ticket", q(5), "end", q(3))
+    last = a[a[:, 7] != 0]
+    if len(last):
+        print("last CTA: enters final sum", round((last[0, 7] - t0) / 1e3, 2), "ends", round((last[0, 3] - t0) / 1e3, 2))
     print("item  prod_start  stage_free  issued   cons_wait  data_in  walk_done   (us from first CTA start)")
     for k in range(64):
         r = it[k]
