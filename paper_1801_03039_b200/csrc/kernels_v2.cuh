@@ -514,7 +514,7 @@ __device__ __forceinline__ void v2_tail_slots(const CountParams& p, const WorkLi
         const uint32_t c0 = (x & 0xffffu) + (g < P_slots ? wl.cnt[g] : 0u);
         const uint32_t c1 = (x >> 16) + (g + 1 < P_slots ? wl.cnt[g + 1] : 0u);
         const uint32_t n0 = __shfl_down_sync(0xffffffffu, c0, GL), n1 = __shfl_down_sync(0xffffffffu, c1, GL);
-        if ((lane & (2 * GL - 1)) == 0 && (c0 | c1 | n0 | n1))
+        if ((lane & (2 * GL - 1)) == 0 && (c0 | c1 | n0 | n1) && p.debug_mode != 5)
             asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
                              stripes + size_t(stripe) * PS4 + ch * CHUNK + (lane / GL) * SPG),
                          "f"(static_cast<float>(c0)), "f"(static_cast<float>(c1)), "f"(static_cast<float>(n0)),
@@ -656,6 +656,19 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
                     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
                                      reinterpret_cast<const unsigned char*>(p.expt) + lo), "r"(n) : "memory");
                 }
+            }
+        }
+        if (pw == 0 && lane == 2 && p.reduce_striped == 2) {
+            // this CTA's share of the slot stripes, so the tail's reductions
+            // (and the release before its ticket) do not wait on DRAM fills
+            const uint64_t bytes = uint64_t(kStripes) * ((P + kV2Pad + 7u) & ~7u) * 4u;
+            const uint64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 127) & ~uint64_t(127);
+            const uint64_t lo = per * blockIdx.x;
+            if (lo < bytes) {
+                const uint32_t n = static_cast<uint32_t>(min(per, bytes - lo) & ~uint64_t(15));
+                if (n)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                                     reinterpret_cast<const unsigned char*>(p.partial) + lo), "r"(n) : "memory");
             }
         }
         const unsigned char* ranks = p.ranks;
