@@ -11,7 +11,8 @@ g++ -std=c++20 -O2 -I include -I $REF -I $JSON tools/probes/ga_phase_probe.cpp "
 g++ -std=c++20 -O2 -I include -I $REF -I $JSON tools/probes/build_gen_compare.cpp "${LINK[@]}" \
   -o tools/probes/build_gen_compare_dropin
 g++ -std=c++20 -O2 -I $REF -I $JSON tools/probes/build_gen_compare.cpp -o tools/probes/build_gen_compare_ref
-for p in graph_update_probe launch_floor_probe gather_probe; do
+g++ -std=c++17 -O2 tools/probes/startup_probe.cpp -ldl -o tools/probes/startup_probe
+for p in graph_update_probe launch_floor_probe gather_probe param_probe; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/probes/$p tools/probes/$p.cu -lcuda
 done
 echo "probes built"

@@ -11,7 +11,7 @@ exe = ROOT / "paper_1801_03039_b200" / "ebic_e2e_driver"
 with tempfile.TemporaryDirectory() as td:
     path = Path(td) / "b.bin"
     with open(path, "wb") as f:
-        for off, cols, counts, fit in t.batches:
+        for off, cols, counts, fit in (t.steady_batches() if sys.argv[1].endswith("ss") else t.batches):
             f.write(np.uint64(len(off) - 1).tobytes()); f.write(off.astype(np.uint64).tobytes())
             f.write(cols.astype(np.uint16).tobytes()); f.write(counts.astype(np.uint64).tobytes())
             f.write(fit.astype(np.float64).tobytes())
