@@ -135,8 +135,9 @@ class ClockSampler:
 
 
 # bytes per matrix cell of the layout the count kernel streams (ebic_ctx_info.layout)
-LAYOUT_CELL_BYTES = {0: 8, 1: 2, 2: 4, 3: 2}
-LAYOUT_NAMES = {0: "fp64", 1: "rank16x1", 2: "rank16x2", 3: "rank16x1c"}
+# (4, 5: one plane packed three rows per 32-bit word, 128 B per 96 rows)
+LAYOUT_CELL_BYTES = {0: 8, 1: 2, 2: 4, 3: 2, 4: 4 / 3, 5: 4 / 3}
+LAYOUT_NAMES = {0: "fp64", 1: "rank16x1", 2: "rank16x2", 3: "rank16x1c", 4: "rank10x3", 5: "rank10x3c"}
 
 
 def algorithmic_bytes(rows: int, off: np.ndarray, cols: np.ndarray, cell_bytes: int) -> int:
@@ -146,7 +147,7 @@ def algorithmic_bytes(rows: int, off: np.ndarray, cols: np.ndarray, cell_bytes: 
     + CBF in + counts/fitness out."""
     P = len(off) - 1
     U = len(np.unique(cols))
-    return rows * U * cell_bytes + (P + 1) * 8 + len(cols) * 2 + P * 8 * 2
+    return round(rows * U * cell_bytes) + (P + 1) * 8 + len(cols) * 2 + P * 8 * 2
 
 
 # ---------------------------------------------------------------------------

@@ -76,7 +76,8 @@ typedef struct ebic_ctx_info {
     size_t device_bytes;  /* matrix bytes resident on shard 0 */
     int sm_count;         /* SMs of shard 0's device */
     int layout;           /* last count launch: 0 fp64 tile, 1/2 = exact rank tile (planes),
-                             3 = one-plane collapsed rank tile (eps > 0) */
+                             3 = one-plane collapsed rank tile (eps > 0), 4/5 = the one-plane
+                             tile (strict / collapsed) packed three rows per 32-bit word */
     int consumer_warps;   /* count-kernel consumer warps per CTA */
 } ebic_ctx_info;
 

@@ -96,7 +96,7 @@ int env_int(const char* name, int dflt) {
 struct Knobs {
     int force_direct, rpg, rpl, stages, ncw, slice, layout_f64, no_collapse, sched_static,
         max_parts, reduce_tree, grid, phase_timing, spg, host_copy, xshard, graph, debug_mode, kernel,
-        gap, compact, v2_np, prefetch;
+        gap, compact, v2_np, prefetch, pack;
     static Knobs from_env() {
         Knobs k;
         k.force_direct = env_int("EBIC_FORCE_DIRECT", 0);
@@ -126,6 +126,8 @@ struct Knobs {
         k.compact = env_int("EBIC_COMPACT", -1);
         k.v2_np = env_int("EBIC_V2_NP", 8);  // K1v2 producer warps (8: 20 consumers; 4: 24)
         k.prefetch = env_int("EBIC_PREFETCH", 0);  // K1v2 compact: L2 prefetch distance (items)
+        // K1v2: one-plane ranks packed three rows per word when they fit 9 bits
+        k.pack = env_int("EBIC_PACK", 1);
         return k;
     }
 };
@@ -189,6 +191,11 @@ struct RankLayout {
     int planes = 0;
     bool collapsed = false;            // one plane tested with <= (eps > 0)
     uint16_t* d = nullptr;
+    // one plane repacked three rows per word (RankWalker<3>), when every rank
+    // fits 9 bits (n_cols <= kPack10MaxCols); K1v2 streams this one
+    uint32_t* d10 = nullptr;
+    size_t d10_bytes = 0;
+    bool packed = false;
     // rows the collapsed layout cannot represent (evaluated exactly in fp64)
     unsigned long long* d_row_excl = nullptr;  // bitmask, ceil(ld / 64) words
     uint32_t* d_excl_rows = nullptr;
@@ -581,16 +588,17 @@ CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int
             c.v2 = 1;
             c.layout = rank_planes;
             c.slice = 128;
-            c.rpg = rank_planes == 2 ? 32 : 64;
-            c.rpl = rank_planes == 2 ? 4 : 8;
+            c.rpg = rank_planes == 3 ? 96 : rank_planes == 2 ? 32 : 64;
+            c.rpl = rank_planes == 3 ? 12 : rank_planes == 2 ? 4 : 8;
             c.ncw = 24;
             c.spg = 2;
             c.stages = kn.stages;  // 0: as many as fit (<= 4)
-            // a lane's 16-bit partial counts grow by <= 8 rows per tile it walks
+            // a lane's 16-bit partial counts grow by <= rpl rows per tile it walks
             const size_t tiles = (s.rows + c.rpg - 1) / c.rpg;
-            if ((tiles / std::max(1, std::min<int>((int)tiles, s.sm_count)) + 2) * 8 <= 0xffff) return c;
+            if ((tiles / std::max(1, std::min<int>((int)tiles, s.sm_count)) + 2) * c.rpl <= 0xffff) return c;
         }
     }
+    if (rank_planes == 3) rank_planes = 1;  // v1: the 16-bit plane
     if (rank_planes) {
         const int want_slice = kn.slice;
         for (int min_stages : {3, 2}) {
@@ -757,6 +765,7 @@ void launch_tma(const CountConfig& c, bool e0, const CUtensorMap& tm, const Coun
 }
 
 constexpr size_t kRankMaxCols = 2048;  // 2C keys sorted in shared memory per row
+constexpr size_t kPack10MaxCols = 510;  // ranks 1..510 + the NaN sentinel in 9 bits
 
 uint64_t eps_key(double eps) {
     if (eps == 0.0) eps = 0.0;  // -0.0 and +0.0 give identical predicates
@@ -842,7 +851,7 @@ RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
             rl.collapsed = true;
             rl.n_excl = (uint32_t)rows.size();
             if (!rows.empty()) {
-                const size_t words = (s.ld + 63) / 64;
+                const size_t words = (s.ld + 63) / 64 + 2;  // K1v2 reads a tile's two words
                 std::vector<unsigned long long> mask(words, 0ull);
                 for (uint32_t r : rows) mask[r / 64] |= 1ull << (r % 64);
                 CK(cudaMalloc(&rl.d_row_excl, words * 8));
@@ -860,6 +869,21 @@ RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
     if (!done) {
         rl.planes = 2;
         launch_rank_build<2, false>(s, n_cols, eps, rl.d, nullptr);
+    }
+    rl.packed = false;
+    if (rl.planes == 1 && n_cols <= kPack10MaxCols && s.knobs.pack && s.knobs.kernel == 2) {
+        const uint32_t tiles = (uint32_t)((s.rows + 95) / 96);
+        const size_t bytes = size_t(tiles) * n_cols * 128;
+        if (rl.d10_bytes < bytes) {
+            if (rl.d10) CK(cudaFree(rl.d10));
+            rl.d10 = nullptr;
+            CK(cudaMalloc(&rl.d10, bytes));
+            rl.d10_bytes = bytes;
+        }
+        rank_pack10_kernel<<<s.sm_count * 8, 256, 0, s.stream>>>(rl.d, (uint32_t)s.ld, (uint32_t)n_cols, tiles,
+                                                               rl.d10);
+        CK(cudaGetLastError());
+        rl.packed = true;
     }
     CK(cudaStreamSynchronize(s.stream));
     rl.ok = true;
@@ -972,14 +996,15 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
     }
     const bool e0 = (eps == 0.0);
     RankLayout* rl = ensure_ranks(s, ctx.n_cols, eps);
-    const int planes = rl ? rl->planes : 0;
+    const int planes = rl ? (rl->packed ? 3 : rl->planes) : 0;
     if (!(s.memo_P == P && s.memo_L == L && s.memo_planes == planes)) {
         s.memo_cfg = choose_config(s, ctx.n_cols, P, L, planes);
         s.memo_P = P, s.memo_L = L, s.memo_planes = planes;
     }
     const CountConfig c = s.memo_cfg;
     if (c.v2) {
-        p.ranks = reinterpret_cast<const unsigned char*>(rl->d);
+        p.ranks = c.layout == 3 ? reinterpret_cast<const unsigned char*>(rl->d10)
+                                : reinterpret_cast<const unsigned char*>(rl->d);
         p.stages = (uint32_t)c.stages;
         p.n_tiles = (uint32_t)((s.rows + c.rpg - 1) / c.rpg);
         const size_t smem = (size_t)s.max_smem - 1024;  // leaves room for the static shared bytes
@@ -1010,7 +1035,14 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         s.last_collapsed = rl->collapsed;
         ensure_partial(s, P, grid, (int)p.reduce_striped);
         p.partial = s.d_partial;
-        if (rl->collapsed) {
+        if (c.layout == 3) {
+            // packed fields: + 0x1ff (strict <) or + 0x200 (<=, collapsed) per field
+            p.rank_k = rl->collapsed ? 0x20080200u : 0x1ff7fdffu;
+            p.row_excl = rl->d_row_excl;
+            p.excl_rows = rl->d_excl_rows;
+            p.excl_vals = rl->d_excl_vals;
+            p.n_excl = rl->n_excl;
+        } else if (rl->collapsed) {
             p.rank_k = 0x80008000u;
             p.row_excl = rl->d_row_excl;
             p.excl_rows = rl->d_excl_rows;
@@ -1025,13 +1057,16 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         const int np = s.knobs.v2_np == 4 ? 4 : 8;
         const int ncw = np == 8 ? 20 : 24;
         const void* fn;
-        if (c.layout == 2)
+        if (c.layout == 3)
+            fn = np == 8 ? reinterpret_cast<const void*>(count_v2_kernel<3, 20, 8>)
+                         : reinterpret_cast<const void*>(count_v2_kernel<3, 24, 4>);
+        else if (c.layout == 2)
             fn = np == 8 ? reinterpret_cast<const void*>(count_v2_kernel<2, 20, 8>)
                          : reinterpret_cast<const void*>(count_v2_kernel<2, 24, 4>);
         else
             fn = np == 8 ? reinterpret_cast<const void*>(count_v2_kernel<1, 20, 8>)
                          : reinterpret_cast<const void*>(count_v2_kernel<1, 24, 4>);
-        static std::atomic<int> v2_smem_set[2][2][64] = {};
+        static std::atomic<int> v2_smem_set[3][2][64] = {};
         std::atomic<int>& flag = v2_smem_set[c.layout - 1][np == 8 ? 1 : 0][s.device & 63];
         if (flag.load(std::memory_order_acquire) < (int)smem) {
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1420,6 +1455,7 @@ void free_shard(Shard& s) {
     cudaFree(s.tables.d_exp);
     for (RankLayout& rl : s.ranks) {
         cudaFree(rl.d);
+        cudaFree(rl.d10);
         cudaFree(rl.d_row_excl);
         cudaFree(rl.d_excl_rows);
         cudaFree(rl.d_excl_vals);
@@ -1630,6 +1666,7 @@ int ebic_ctx_get_info(const ebic_ctx* ctx, ebic_ctx_info* info) {
         info->sm_count = s.sm_count;
         info->layout = s.last_cfg.layout;
         if (s.last_cfg.layout == 1 && s.last_collapsed) info->layout = 3;
+        if (s.last_cfg.layout == 3) info->layout = s.last_collapsed ? 5 : 4;  // packed 10-bit fields
         info->consumer_warps = s.last_cfg.ncw == 32 ? 31 : s.last_cfg.ncw;
     });
 }

@@ -840,13 +840,24 @@ struct F64Walker {
 //     lo'[4] then hi'[4] (16 bytes); a lane owns 4 rows (one LDS.128).
 //   PLANES == 1 (eps == 0, no NaN): lo == hi, one u16 per cell; a lane owns
 //     8 rows (one LDS.128).
-// Tile: 128 bytes per column (32 rows x 2 planes, or 64 rows x 1 plane).
+//   PLANES == 3 (K1v2 only; one plane whose ranks fit 9 bits, i.e. at most
+//     510 distinct values per row): three rows per 32-bit word in 10-bit
+//     fields (r' = r | 0x200, bits 0-9 / 10-19 / 20-29, row 3w + f of the
+//     tile in field f of word w), so the same IADD3 + LOP3 tests three rows:
+//         ok &= cur' - prev' + 0x1ff7fdff     (bits 9 / 19 / 29)
+//     (each field of the sum is in [0, 0x3fe]: no carry between fields).
+//     A lane owns 12 consecutive rows (one LDS.128), a tile 96 rows: a third
+//     fewer bytes per row to stream, stage and test than one 16-bit plane.
+// Tile: 128 bytes per column (32 rows x 2 planes, 64 rows x 1 plane, or 96
+// packed rows).
 // ---------------------------------------------------------------------------
 template <int PLANES, int SLICE, int SPG = 2>
 struct RankWalker {
     static_assert(SLICE == 64 || SLICE == 128, "column slice of 64 or 128 bytes");
-    static constexpr int kRowsPerLane = PLANES == 2 ? 4 : 8;
-    static constexpr int kRowsPerTile = SLICE / (2 * PLANES);
+    static_assert(PLANES != 3 || SLICE == 128, "packed ranks: 128-byte slices");
+    static constexpr bool kPacked = PLANES == 3;
+    static constexpr int kRowsPerLane = kPacked ? 12 : PLANES == 2 ? 4 : 8;
+    static constexpr int kRowsPerTile = kPacked ? 96 : SLICE / (2 * PLANES);
     static constexpr int kLaneBytes = 16;
     static constexpr int kColBytes = SLICE;
     static constexpr int kShift = SLICE == 128 ? 7 : 6;
@@ -855,7 +866,7 @@ struct RankWalker {
     // one column's rows, [block][column][64 u16]; a 64-byte slice is half a block.
     static constexpr bool kTileMajor = true;
     static constexpr int kSlicesPerBlock = 128 / SLICE;
-    static constexpr int kWords = kRowsPerLane / 2;           // ok words per lane
+    static constexpr int kWords = kPacked ? 4 : kRowsPerLane / 2;  // ok words per lane
     static constexpr int kSeriesPerGroup = SPG;               // independent walks per group
     static constexpr int kFieldBits = 32 / SPG;               // packed per-series counts
     static_assert(SPG == 2 || SPG == 4, "2 or 4 series per lane group");
@@ -871,6 +882,15 @@ struct RankWalker {
                                                  uint32_t kconst) {
         Mask v;
         v.m = 0;
+        if (kPacked) {  // row 3k + f: bit 9 + 10 f of word k, folded down by k
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int f = 0; f < 3; ++f)
+                    if (row0 + 3 * k + f < n_rows && !((excl >> (3 * k + f)) & 1u)) v.m |= (1u << (9 + 10 * f)) >> k;
+            v.k = kconst;
+            return v;
+        }
 #pragma unroll
         for (int k = 0; k < kWords; ++k)
             v.m |= (((row0 + 2 * k < n_rows && !((excl >> (2 * k)) & 1u)) ? 0x8000u : 0u) |
@@ -915,7 +935,7 @@ struct RankWalker {
         }
     }
     __device__ __forceinline__ static uint32_t tally(const uint32_t* ok, const Mask& vm) {
-        constexpr uint32_t kRes = 0x80008000u;  // result bits of an ok word
+        constexpr uint32_t kRes = kPacked ? 0x20080200u : 0x80008000u;  // result bits of an ok word
         uint32_t f = ok[0] & kRes;
 #pragma unroll
         for (int k = 1; k < kWords; ++k) f |= (ok[k] & kRes) >> k;
@@ -1467,6 +1487,34 @@ __global__ void __launch_bounds__(256)
         out[at(c, plane)] = v;
     }
     if (COLLAPSED && tid == 0) dirty_out[r] = static_cast<uint8_t>(s_dirty);
+}
+
+// One-plane 16-bit rank matrix (tile-major, 64-row blocks) -> the packed
+// layout of RankWalker<3>: [tile][column][32 words], 96 rows per tile, row
+// 3w + f in bits 10f..10f+9 of word w.  A cell r' = 0x8000 | r (r <= 0x1fe)
+// becomes 0x200 | r, the NaN sentinel 0xffff becomes 0x3ff (above every
+// rank, as 0xffff is), rows past the matrix 0x200 (masked by the kernel).
+__global__ void rank_pack10_kernel(const uint16_t* __restrict__ in, uint32_t in_rows, uint32_t n_cols,
+                                   uint32_t n_tiles, uint32_t* __restrict__ out) {
+    const size_t n = size_t(n_tiles) * n_cols * 32;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = static_cast<uint32_t>(i & 31);
+        const size_t tc = i >> 5;
+        const uint32_t c = static_cast<uint32_t>(tc % n_cols);
+        const uint32_t t = static_cast<uint32_t>(tc / n_cols);
+        uint32_t x = 0;
+#pragma unroll
+        for (int f = 0; f < 3; ++f) {
+            const uint32_t r = t * 96 + 3 * w + f;
+            uint32_t v = 0x200u;
+            if (r < in_rows) {
+                const uint32_t u = in[(size_t(r / 64) * n_cols + c) * 64 + (r % 64)];
+                v = u == 0xffffu ? 0x3ffu : (0x200u | (u & 0x1ffu));
+            }
+            x |= v << (10 * f);
+        }
+        out[i] = x;
+    }
 }
 
 // Row-major copy of selected rows of the column-major matrix (one CTA per row).

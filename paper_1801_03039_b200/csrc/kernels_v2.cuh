@@ -49,7 +49,7 @@ struct V2Layout {
     uint32_t runs, run_slot;  // u32[max_runs] each
     uint32_t acc;       // u32[n_chunks][32] per-lane partial counts
     uint32_t colw;      // u32[4][64] run-start / run-end word masks and prefix counts
-    uint32_t excl;      // u64[kV2ExclItems] excl words of the CTA's items
+    uint32_t excl;      // u64[2][kV2ExclItems] excl words of the CTA's items (a tile spans <= 2)
     uint32_t area;      // first byte of the stage area (128-aligned)
 };
 
@@ -83,7 +83,7 @@ __host__ __device__ inline V2Layout v2_layout(uint32_t P0, uint32_t L0, uint32_t
     v.run_slot = at; at = up16(at + 4 * v2_max_runs(n_cols));
     v.acc = at;      at = up16(at + 4 * 32 * ((P + kV2Chunk - 1) / kV2Chunk));
     v.colw = at;     at = up16(at + 4 * 4 * 64);
-    v.excl = at;     at = up16(at + 8 * kV2ExclItems);
+    v.excl = at;     at = up16(at + 16 * kV2ExclItems);
     v.area = (at + 127u) & ~127u;
     return v;
 }
@@ -252,12 +252,16 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
     unsigned long long* excl_items = reinterpret_cast<unsigned long long*>(smem + v.excl);
     if (p.row_excl && tid < kV2ExclItems) {
         const uint32_t item = blockIdx.x + tid * gridDim.x;
-        unsigned long long x = 0ull;
+        unsigned long long x0 = 0ull, x1 = 0ull;
         if (item < n_items) {
+            // the host pads the mask with two zero words past the last tile
             const uint32_t tile = item < full ? item : full + (item - full) / parts;
-            x = __ldg(p.row_excl + ((tile * rows_per_tile) >> 6));
+            const unsigned long long* w = p.row_excl + ((tile * rows_per_tile) >> 6);
+            x0 = __ldg(w);
+            x1 = __ldg(w + 1);
         }
-        excl_items[tid] = x;
+        excl_items[2 * tid] = x0;
+        excl_items[2 * tid + 1] = x1;
     }
     const uint32_t nblk = (P + 31) / 32;
     const int lane = tid & 31, nw = nthreads >> 5;
@@ -557,7 +561,8 @@ __device__ __forceinline__ void v2_tail_slots(const CountParams& p, const WorkLi
 }
 
 // ---------------------------------------------------------------------------
-// K1v2.  PLANES: 1 (64-row tiles) or 2 (32-row tiles); 128-byte slices.
+// K1v2.  PLANES: 1 (64-row tiles), 2 (32-row tiles) or 3 (one plane packed
+// three rows per word, 96-row tiles); 128-byte slices.
 // Grid: persistent, <= SMs; block: NCW consumer + NP producer warps.
 // p.compact: stage the launch's referenced columns (runs); else whole tiles,
 // one contiguous bulk copy each (short launches: no wait for the column set).
@@ -566,7 +571,7 @@ template <int PLANES, int NCW, int NP>
 __global__ void __launch_bounds__((NCW + NP) * 32, 1)
     count_v2_kernel(const __grid_constant__ CountParams p) {
     using W = RankWalker<PLANES, 128, 2>;
-    constexpr int RPG = W::kRowsPerTile;  // 64 or 32
+    constexpr int RPG = W::kRowsPerTile;  // 64, 32 or 96
     constexpr int RPL = W::kRowsPerLane;
     constexpr int GL = RPG / RPL;         // 8 lanes per group
     constexpr int GW = 32 / GL;           // 4 groups per warp
@@ -829,8 +834,18 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
             const uint32_t r0 = tile * RPG + gl * RPL;
             uint32_t excl = 0;
             if (p.row_excl) {
-                const unsigned long long w = it < kV2ExclItems ? excl_items[it] : __ldg(p.row_excl + (r0 >> 6));
-                excl = static_cast<uint32_t>(w >> (r0 & 63)) & ((1u << RPL) - 1u);
+                // the lane's RPL rows within the tile's two mask words
+                const uint32_t wb = (tile * RPG) >> 6, sh = r0 - 64u * wb;
+                unsigned long long w0, w1;
+                if (it < kV2ExclItems) {
+                    w0 = excl_items[2 * it];
+                    w1 = excl_items[2 * it + 1];
+                } else {
+                    w0 = __ldg(p.row_excl + wb);
+                    w1 = __ldg(p.row_excl + wb + 1);
+                }
+                const unsigned long long win = sh >= 64 ? w1 >> (sh - 64) : sh ? (w0 >> sh) | (w1 << (64 - sh)) : w0;
+                excl = static_cast<uint32_t>(win) & ((1u << RPL) - 1u);
             }
             if (p.debug_mode != 3) mbar_wait(&full_bar[st], phase);
             const uint32_t base = area_addr + st * stage_bytes;

@@ -30,7 +30,8 @@ KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NCW="24"), dict(EBIC_N
                   [dict(EBIC_LAYOUT_F64="1", EBIC_NCW="16"), dict(EBIC_LAYOUT_F64="1", EBIC_NCW="32"), dict(EBIC_FORCE_DIRECT="1")] +
                   # K1v2 (default for rank layouts) vs the v1 tile kernel, and K1v2's own knobs
                   [dict(EBIC_KERNEL="1"), dict(EBIC_KERNEL="1", EBIC_NO_COLLAPSE="1"), dict(EBIC_COMPACT="1"), dict(EBIC_COMPACT="0"),
-                   dict(EBIC_COMPACT="1", EBIC_GAP="2"), dict(EBIC_STAGES="1"), dict(EBIC_COMPACT="1", EBIC_NO_COLLAPSE="1")])
+                   dict(EBIC_COMPACT="1", EBIC_GAP="2"), dict(EBIC_STAGES="1"), dict(EBIC_COMPACT="1", EBIC_NO_COLLAPSE="1"),
+                   dict(EBIC_PACK="0"), dict(EBIC_PACK="0", EBIC_COMPACT="1")])
 
 
 @contextmanager
@@ -197,6 +198,38 @@ def test_v2_column_runs_vs_oracle(cfg):
                         got = ev.count_matches(pop, eps)
                         want = port.count_matches(v, pop.offsets, pop.col_indices, eps)
                         assert (got == want).all(), (rows, name, eps)
+
+
+PACK_CONFIGS = [dict(), dict(EBIC_COMPACT="1"), dict(EBIC_COMPACT="0"), dict(EBIC_GRID="7"),
+                dict(EBIC_COMPACT="1", EBIC_GRID="7"), dict(EBIC_STAGES="1"), dict(EBIC_V2_NP="4")]
+
+
+@pytest.mark.parametrize("cfg", PACK_CONFIGS, ids=lambda d: "-".join(f"{k}={v}" for k, v in d.items()) or "default")
+def test_v2_packed_ranks_vs_oracle(cfg):
+    """Matrices of <= 510 columns stream one rank plane packed three rows per
+    word (96-row tiles, 10-bit fields): ragged row counts around the 96-row
+    tile and 64-row mask-word boundaries, the widest packable matrix, ties,
+    strict and collapsed tests, dirty rows straddling two mask words."""
+    rng = np.random.default_rng(33)
+    with env(**cfg):
+        for rows, n_cols in ((1, 5), (95, 40), (96, 40), (97, 40), (191, 510), (1000, 510), (13000, 300),
+                             (4097, 97)):
+            v = np.round(rng.standard_normal((rows, n_cols)), 1)  # many ties
+            for r in rng.choice(rows, size=min(rows, 9), replace=False):  # eps-close pairs: dirty rows
+                a, b = rng.choice(n_cols, size=2, replace=False) if n_cols > 1 else (0, 0)
+                v[r, b] = v[r, a] + 0.5e-6
+            series = random_population(rng, n_cols, 600, max_len=12)
+            pop = cbf(series)
+            with eb.Evaluator(v) as ev:
+                for eps in (0.0, 1e-6, 0.05):
+                    got = ev.count_matches(pop, eps)
+                    want = port.count_matches(v, pop.offsets, pop.col_indices, eps)
+                    assert (got == want).all(), (rows, n_cols, eps)
+                    if eps == 0.0:
+                        assert ev.info().layout == 4, ev.info().layout
+                f = ev.evaluate_population(pop, eb.FitnessParams(max(4, rows // 50)), 1e-6)
+                _, wf = port.evaluate_population(v, pop.offsets, pop.col_indices, max(4, rows // 50), 1e-6)
+                assert bits_equal(f, wf)
 
 
 @pytest.mark.parametrize("cfg", [dict(), dict(EBIC_COMPACT="1"), dict(EBIC_KERNEL="1")], ids=str)
@@ -398,7 +431,8 @@ def test_collapsed_rank_layout_with_dirty_rows(n_dirty):
             _, wf = port.evaluate_population(v, pop.offsets, pop.col_indices, 120, e)
             assert bits_equal(f, wf)
         info = ev.info()
-    assert info.layout == (3 if n_dirty <= 64 else 2)
+    # 5: the collapsed plane packed three rows per word (n_cols <= 510)
+    assert info.layout == (5 if n_dirty <= 64 else 2)
 
 
 @pytest.mark.parametrize("cfg", [dict(), dict(EBIC_NO_COLLAPSE="1"), dict(EBIC_LAYOUT_F64="1"),
