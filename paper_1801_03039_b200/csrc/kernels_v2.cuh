@@ -73,7 +73,7 @@ __host__ __device__ inline V2Layout v2_layout(uint32_t P0, uint32_t L0, uint32_t
     v.sl = at;       at = up16(at + 4 * P);
     v.slen = at;     at = up16(at + 4 * P);
     v.sstart = at;   at = up16(at + 4 * P);
-    v.cnt = at;      at = up16(at + 4 * (P + 2));
+    v.cnt = at;      at = up16(at + 4 * (P + 4));  // + read as whole quads by the tail
     v.cdesc = at;    at = up16(at + 4 * ((P + kV2Chunk - 1) / kV2Chunk));
     v.pcols = at;    at = up16(at + 4 * (L + 3 * P));
     v.bm = at;       at += 64 * 4;
@@ -289,7 +289,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
     }
     for (uint32_t i = tid; i < nblk * kLenBuckets; i += nthreads) w.wh[i] = 0;
     for (int b = tid; b < kLenBuckets; b += nthreads) w.hist[b] = 0;
-    for (uint32_t i = tid; i < P + kV2Pad + 2; i += nthreads) w.cnt[i] = 0;
+    for (uint32_t i = tid; i < P + kV2Pad + 4; i += nthreads) w.cnt[i] = 0;
     {
         uint32_t* acc = reinterpret_cast<uint32_t*>(smem + v.acc);
         const uint32_t n_acc = 32u * ((P + kV2Pad + CHUNK - 1) / CHUNK);
@@ -506,23 +506,30 @@ __device__ __forceinline__ void v2_tail_slots(const CountParams& p, const WorkLi
     float* stripes = reinterpret_cast<float*>(p.partial);
     const uint32_t stripe = blockIdx.x % kStripes;
     unsigned long long* stamp = p.phase_ns ? p.phase_ns + 8ull * blockIdx.x : nullptr;
-    const int nwarps = blockDim.x >> 5;
-    const uint32_t n_chunks = (P_slots + CHUNK - 1) / CHUNK;
-    for (uint32_t ch = warp; ch < n_chunks; ch += nwarps) {
-        uint32_t x = acc[ch * 32 + lane];
+    // One thread per 4 consecutive slots: chunk q / 2, lane groups 2 (q % 2)
+    // and 2 (q % 2) + 1 -- sixteen consecutive per-lane words (low / high
+    // halves: the group's two slots), summed unpacked, plus the fp64 fix-up
+    // rows, out as one 4-wide reduction.
+    (void)warp, (void)lane;
+    const uint32_t n_quads = (P_slots + 3) / 4;
+    for (uint32_t q = threadIdx.x; q < n_quads; q += blockDim.x) {
+        const uint4* a4 = reinterpret_cast<const uint4*>(acc + (q >> 1) * 32 + (q & 1) * 2 * GL);
+        uint32_t c[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int o = GL / 2; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        // lane 8k holds slots 2k, 2k+1 of the chunk; gather 4 slots per lane
-        // 0 (slots 0-3) and lane 16 (slots 4-7)
-        const uint32_t g = ch * CHUNK + (lane / GL) * SPG;
-        const uint32_t c0 = (x & 0xffffu) + (g < P_slots ? wl.cnt[g] : 0u);
-        const uint32_t c1 = (x >> 16) + (g + 1 < P_slots ? wl.cnt[g + 1] : 0u);
-        const uint32_t n0 = __shfl_down_sync(0xffffffffu, c0, GL), n1 = __shfl_down_sync(0xffffffffu, c1, GL);
-        if ((lane & (2 * GL - 1)) == 0 && (c0 | c1 | n0 | n1) && p.debug_mode != 5)
+        for (int i = 0; i < 4; ++i) {
+            const uint4 w = a4[i];
+            const int h = 2 * (i >> 1);  // group 2 (q % 2) for words 0-7, the next for 8-15
+            c[h] += (w.x & 0xffffu) + (w.y & 0xffffu) + (w.z & 0xffffu) + (w.w & 0xffffu);
+            c[h + 1] += (w.x >> 16) + (w.y >> 16) + (w.z >> 16) + (w.w >> 16);
+        }
+        const uint32_t g = 4 * q;
+        const uint4 f = *reinterpret_cast<const uint4*>(wl.cnt + g);  // zero past P_slots
+        c[0] += f.x, c[1] += f.y, c[2] += f.z, c[3] += f.w;
+        if ((c[0] | c[1] | c[2] | c[3]) && p.debug_mode != 5)
             asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(
-                             stripes + size_t(stripe) * PS4 + ch * CHUNK + (lane / GL) * SPG),
-                         "f"(static_cast<float>(c0)), "f"(static_cast<float>(c1)), "f"(static_cast<float>(n0)),
-                         "f"(static_cast<float>(n1))
+                             stripes + size_t(stripe) * PS4 + g),
+                         "f"(static_cast<float>(c[0])), "f"(static_cast<float>(c[1])), "f"(static_cast<float>(c[2])),
+                         "f"(static_cast<float>(c[3]))
                          : "memory");
     }
     __shared__ int s_last;
@@ -903,15 +910,19 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
         __syncthreads();
         const uint32_t P_slots = misc[3];
         for (uint32_t ch = warp; ch < (P_slots + CHUNK - 1) / CHUNK; ch += nwarps) {
-            uint32_t x = acc[ch * 32 + lane];
+            // the two 16-bit halves summed apart: a CTA's count may pass 2^16
+            uint32_t x = acc[ch * 32 + lane], lo = x & 0xffffu, hi = x >> 16;
 #pragma unroll
-            for (int o = GL / 2; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+            for (int o = GL / 2; o >= 1; o >>= 1) {
+                lo += __shfl_xor_sync(0xffffffffu, lo, o);
+                hi += __shfl_xor_sync(0xffffffffu, hi, o);
+            }
             const uint32_t g0 = ch * CHUNK + grp * SPG;
             if (gl == 0) {
 #pragma unroll
                 for (int q = 0; q < SPG; ++q) {
                     const uint32_t s = g0 + q < P_slots ? wl.sl[g0 + q] : 0xffffffffu;
-                    if (s != 0xffffffffu) by_series[s] = wl.cnt[g0 + q] + ((x >> (16 * q)) & 0xffffu);
+                    if (s != 0xffffffffu) by_series[s] = wl.cnt[g0 + q] + (q ? hi : lo);
                 }
             }
         }
