@@ -746,7 +746,8 @@ def run_ours(args):
                     "algorithmic_bytes_per_launch": avg_bytes,
                     "layout": LAYOUT_NAMES[layout], "cell_bytes": LAYOUT_CELL_BYTES[layout],
                     "peak_source": peak_src,
-                    "kernel": "count_tma_kernel (fused Eq. 1 epilogue)",
+                    "kernel": ("count_tma_kernel (v1, fused Eq. 1 epilogue)" if os.environ.get("EBIC_KERNEL") == "1"
+                               else "count_v2_kernel (K1v2, fused Eq. 1 epilogue)"),
                     "avg_launch_us": avg_launch_ms * 1e3}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
