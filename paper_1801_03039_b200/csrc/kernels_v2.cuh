@@ -369,8 +369,22 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
                 const bool uni = g + CHUNK <= end && len >= 2 && len <= 12;
                 reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = uni ? ((st << 8) | len) : 0u;
             }
-            // owner of each 4-entry quad of the list (filled quad-parallel below)
-            for (uint32_t q = 0; q < pad4(len) / 4; ++q) owner[st / 4 + q] = static_cast<uint16_t>(g);
+            if (compact) {
+                // owner of each 4-entry quad of the list (filled quad-parallel below)
+                for (uint32_t q = 0; q < pad4(len) / 4; ++q) owner[st / 4 + q] = static_cast<uint16_t>(g);
+            } else {
+                // whole tiles: a column's slot is the column itself, so the
+                // lane writes its series' list now (no second pass, no barrier)
+                const uint16_t* from = w.raw + w.rel[s];
+                for (uint32_t q = 0; q < pad4(len) / 4; ++q) {
+                    uint4 o;
+                    o.x = from[4 * q] * 128u;
+                    o.y = 4 * q + 1 < len ? from[4 * q + 1] * 128u : 0u;
+                    o.z = 4 * q + 2 < len ? from[4 * q + 2] * 128u : 0u;
+                    o.w = 4 * q + 3 < len ? from[4 * q + 3] * 128u : 0u;
+                    reinterpret_cast<uint4*>(w.pcols)[st / 4 + q] = o;
+                }
+            }
         }
     }
     if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 601] = global_ns();
@@ -387,19 +401,22 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
         w.sl[g] = 0xffffffffu;
         w.slen[g] = b;
         w.sstart[g] = st;
-        for (uint32_t q = 0; q < pad4(b) / 4; ++q) owner[st / 4 + q] = static_cast<uint16_t>(g);
+        for (uint32_t q = 0; q < pad4(b) / 4; ++q) {
+            if (compact) owner[st / 4 + q] = static_cast<uint16_t>(g);
+            else reinterpret_cast<uint4*>(w.pcols)[st / 4 + q] = make_uint4(0u, 0u, 0u, 0u);
+        }
         if (g % CHUNK == 0)
             reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = (b >= 2 && b <= 12) ? ((st << 8) | b) : 0u;
     }
     if (tid == 0) reinterpret_cast<uint32_t*>(smem + v.misc)[3] = pslots;
     if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 601 + 1] = global_ns();
-    named_bar_sync(bar_id, nthreads);  // 4a
-    if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 601 + 2] = global_ns();
-    // The lists of buckets < 63, four entries per thread: slot byte offsets
-    // of the series' columns, zero past its length (and for dummies).  A
-    // series-per-thread fill would leave the longest series on the critical
-    // path.
-    {
+    // Compacted staging: the lists of buckets < 63, four entries per thread:
+    // slot byte offsets of the series' columns, zero past its length (and for
+    // dummies).  A series-per-thread fill would leave the longest series (and
+    // its slot look-ups) on the critical path.
+    if (compact) {
+        named_bar_sync(bar_id, nthreads);  // 4a
+        if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 601 + 2] = global_ns();
         const uint32_t n_quads = w.hpad[kLenBuckets - 1] / 4;
         for (uint32_t j = tid; j < n_quads; j += nthreads) {
             const uint32_t g = owner[j];
@@ -422,7 +439,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
 
     const uint32_t ovf = w.hist[kLenBuckets - 1];
     const uint32_t P_slots = pslots;
-    if (ovf < P_slots) {
+    if (ovf < P_slots) {  // series of 63+ columns (uniform branch)
         if (tid == 0) {
             uint32_t run = w.hpad[kLenBuckets - 1];
             for (uint32_t g = ovf; g < P_slots; ++g) {
@@ -437,12 +454,13 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
             for (uint32_t i = 0; i < pad4(len); ++i)
                 w.pcols[st + i] = i < len ? slot_of(from[i]) * 128u : 0u;
         }
+        // their chunks take the per-slot path (the chunk holding slot ovf - 1,
+        // if shared, already has descriptor 0: it ends past its bucket)
+        uint32_t* cdesc = reinterpret_cast<uint32_t*>(smem + v.cdesc);
+        for (uint32_t ch = (ovf + CHUNK - 1) / CHUNK + tid; ch < (P_slots + CHUNK - 1) / CHUNK; ch += nthreads)
+            cdesc[ch] = 0u;
+        named_bar_sync(bar_id, nthreads);  // 5
     }
-    // overflow-bucket chunks (lengths >= 63) take the per-slot path
-    uint32_t* cdesc = reinterpret_cast<uint32_t*>(smem + v.cdesc);
-    for (uint32_t ch = (ovf + CHUNK - 1) / CHUNK + tid; ch < (P_slots + CHUNK - 1) / CHUNK; ch += nthreads) cdesc[ch] = 0u;
-    if (ovf % CHUNK && tid == 0) cdesc[ovf / CHUNK] = 0u;
-    named_bar_sync(bar_id, nthreads);  // 5
     if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 600 + 5] = global_ns();
 }
 
