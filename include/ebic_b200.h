@@ -79,6 +79,8 @@ typedef struct ebic_ctx_info {
                              3 = one-plane collapsed rank tile (eps > 0), 4/5 = the one-plane
                              tile (strict / collapsed) packed three rows per 32-bit word */
     int consumer_warps;   /* count-kernel consumer warps per CTA */
+    int kernel;           /* last count launch: 1 = v1 tile or direct kernel, 2 = K1v2
+                             (row tiles per CTA), 3 = K1s (series per CTA) */
 } ebic_ctx_info;
 
 /* Library / device queries. */

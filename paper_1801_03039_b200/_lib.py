@@ -35,6 +35,7 @@ class CtxInfo(C.Structure):
         ("sm_count", C.c_int),
         ("layout", C.c_int),
         ("consumer_warps", C.c_int),
+        ("kernel", C.c_int),
     ]
 
 

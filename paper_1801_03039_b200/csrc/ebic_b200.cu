@@ -35,6 +35,7 @@
 #include "../../include/ebic_b200.h"
 #include "kernels.cuh"
 #include "kernels_v2.cuh"
+#include "kernels_s.cuh"
 
 using namespace ebic_b200;
 
@@ -96,7 +97,7 @@ int env_int(const char* name, int dflt) {
 struct Knobs {
     int force_direct, rpg, rpl, stages, ncw, slice, layout_f64, no_collapse, sched_static,
         max_parts, reduce_tree, grid, phase_timing, spg, host_copy, xshard, graph, debug_mode, kernel,
-        gap, compact, v2_np, prefetch, pack;
+        gap, compact, v2_np, prefetch, pack, split;
     static Knobs from_env() {
         Knobs k;
         k.force_direct = env_int("EBIC_FORCE_DIRECT", 0);
@@ -128,6 +129,8 @@ struct Knobs {
         k.prefetch = env_int("EBIC_PREFETCH", 0);  // K1v2 compact: L2 prefetch distance (items)
         // K1v2: one-plane ranks packed three rows per word when they fit 9 bits
         k.pack = env_int("EBIC_PACK", 1);
+        // K1s (series-split kernel) for short single-shard launches: -1 auto, 0 off, 1 always
+        k.split = env_int("EBIC_SPLIT", -1);
         return k;
     }
 };
@@ -255,6 +258,7 @@ struct Shard {
     cudaStream_t cur_stream = nullptr;
     cudaEvent_t switch_event = nullptr;
     bool last_collapsed = false;
+    int last_kernel = 0;  // 1 v1 tile / direct, 2 K1v2, 3 K1s
     // choose_config memo (same P / L / layout as the previous launch)
     size_t memo_P = 0, memo_L = 0;
     int memo_planes = -1;
@@ -310,7 +314,8 @@ void grow_pinned(unsigned char** p, size_t* cap, size_t need) {
 // mode: 0 tree, 1 u32 stripes [P][8], 2 fp32 stripes [8][P rounded to 4] (K1v2)
 void ensure_partial(Shard& s, size_t P, int grid, int mode) {
     const size_t gsz = reduce_group_size((uint32_t)grid);
-    const size_t need = mode == 2 ? ((P + kV2Pad + 7) & ~size_t(7)) * kStripes  // slots incl. dummies, whole chunks
+    const size_t need = mode == 3 ? 2 * P  // K1s: split-series counts + arrival counters
+                        : mode == 2 ? ((P + kV2Pad + 7) & ~size_t(7)) * kStripes  // slots incl. dummies, whole chunks
                         : mode == 1 ? P * kStripes : (size_t(grid) + (grid + gsz - 1) / gsz) * P;
     if (need <= s.partial_cap && mode == s.last_reduce) return;
     // a launch still queued on the previous stream may use the old scratch
@@ -766,6 +771,7 @@ void launch_tma(const CountConfig& c, bool e0, const CUtensorMap& tm, const Coun
 
 constexpr size_t kRankMaxCols = 2048;  // 2C keys sorted in shared memory per row
 constexpr size_t kPack10MaxCols = 510;  // ranks 1..510 + the NaN sentinel in 9 bits
+constexpr double kSplitMaxL2Bytes = 4e6;  // K1s while rows x sum(len) x b stays below this (measured crossover: C1 1.6 MB K1s faster, C3 17 MB K1v2 faster)
 
 uint64_t eps_key(double eps) {
     if (eps == 0.0) eps = 0.0;  // -0.0 and +0.0 give identical predicates
@@ -1030,10 +1036,19 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         p.compact = compact ? 1u : 0u;
         if (!compact) p.stages = full_stages;
         p.prefetch = compact ? (uint32_t)std::max(0, s.knobs.prefetch) : 0u;
-        s.last_grid = grid;
+        // K1s (kernels_s.cuh) for short single-shard launches: every CTA takes
+        // whole series over all rows, reading its columns' slices through L2
+        // (rows x sum(len) x b bytes) -- no length sort, no cross-CTA sum
+        const int sgrid = s.knobs.grid > 0 ? s.knobs.grid : 2 * s.sm_count;
+        const double cell = c.layout == 3 ? 4.0 / 3.0 : c.layout == 2 ? 4.0 : 2.0;
+        const bool use_s = !xacc && L <= size_t(kSMaxMine) * (size_t)sgrid &&
+                           (s.knobs.split == 1 ||
+                            (s.knobs.split < 0 && !long_launch && double(s.rows) * L * cell <= kSplitMaxL2Bytes));
+        s.last_grid = use_s ? sgrid : grid;
         s.last_cfg = c;
         s.last_collapsed = rl->collapsed;
-        ensure_partial(s, P, grid, (int)p.reduce_striped);
+        s.last_kernel = use_s ? 3 : 2;
+        ensure_partial(s, P, use_s ? sgrid : grid, use_s ? 3 : (int)p.reduce_striped);
         p.partial = s.d_partial;
         if (c.layout == 3) {
             // packed fields: + 0x1ff (strict <) or + 0x200 (<=, collapsed) per field
@@ -1050,6 +1065,24 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
             p.n_excl = rl->n_excl;
         } else {
             p.rank_k = 0x7fff7fffu;
+        }
+        if (use_s) {
+            const void* fs = c.layout == 3   ? reinterpret_cast<const void*>(count_s_kernel<3>)
+                             : c.layout == 2 ? reinterpret_cast<const void*>(count_s_kernel<2>)
+                                             : reinterpret_cast<const void*>(count_s_kernel<1>);
+            s.last_cfg.ncw = kSThreads / 32;
+            s.last_cfg.stages = 0;
+            void* args[1] = {const_cast<CountParams*>(&p)};
+            const size_t ssmem = (P + 1 + L) * sizeof(uint32_t);  // offsets + my column lists (<= L)
+            static std::atomic<int> s_smem_set[3][64] = {};
+            std::atomic<int>& sflag = s_smem_set[c.layout - 1][s.device & 63];
+            if (ssmem > 48 * 1024 && sflag.load(std::memory_order_acquire) < (int)ssmem) {
+                CK(cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+                sflag.store((int)ssmem, std::memory_order_release);
+            }
+            launch_kernel(&s, fs, sgrid, kSThreads, ssmem, st, args);
+            CK(cudaGetLastError());
+            return;
         }
         // warps: 20 consumers + 8 producers (default: eight warps' lanes issue
         // the compacted runs' bulk copies, 1.7 us per C5 tile against 2.9 us
@@ -1091,6 +1124,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         const int g_env = s.knobs.grid;
         if (g_env > 0) grid = std::min<int>(g_env, (int)p.n_tiles);
         s.last_grid = grid;
+        s.last_kernel = 1;
         s.last_cfg = c;
         s.last_collapsed = c.layout && rl->collapsed;
         ensure_partial(s, P, grid, (int)p.reduce_striped);
@@ -1115,6 +1149,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         }
         const int grid = (int)((s.rows + 255) / 256);
         s.last_grid = grid;
+        s.last_kernel = 1;
         s.last_cfg = c;
         s.last_collapsed = false;
         ensure_partial(s, P, grid, (int)p.reduce_striped);
@@ -1668,6 +1703,7 @@ int ebic_ctx_get_info(const ebic_ctx* ctx, ebic_ctx_info* info) {
         if (s.last_cfg.layout == 1 && s.last_collapsed) info->layout = 3;
         if (s.last_cfg.layout == 3) info->layout = s.last_collapsed ? 5 : 4;  // packed 10-bit fields
         info->consumer_warps = s.last_cfg.ncw == 32 ? 31 : s.last_cfg.ncw;
+        info->kernel = s.last_kernel;
     });
 }
 

@@ -882,7 +882,7 @@ struct RankWalker {
                                                  uint32_t kconst) {
         Mask v;
         v.m = 0;
-        if (kPacked) {  // row 3k + f: bit 9 + 10 f of word k, folded down by k
+        if constexpr (kPacked) {  // row 3k + f: bit 9 + 10 f of word k, folded down by k
 #pragma unroll
             for (int k = 0; k < 4; ++k)
 #pragma unroll

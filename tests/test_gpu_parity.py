@@ -31,7 +31,11 @@ KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NCW="24"), dict(EBIC_N
                   # K1v2 (default for rank layouts) vs the v1 tile kernel, and K1v2's own knobs
                   [dict(EBIC_KERNEL="1"), dict(EBIC_KERNEL="1", EBIC_NO_COLLAPSE="1"), dict(EBIC_COMPACT="1"), dict(EBIC_COMPACT="0"),
                    dict(EBIC_COMPACT="1", EBIC_GAP="2"), dict(EBIC_STAGES="1"), dict(EBIC_COMPACT="1", EBIC_NO_COLLAPSE="1"),
-                   dict(EBIC_PACK="0"), dict(EBIC_PACK="0", EBIC_COMPACT="1")])
+                   dict(EBIC_PACK="0"), dict(EBIC_PACK="0", EBIC_COMPACT="1"),
+                   # K1s (series per CTA; default for short launches) against K1v2, and its shapes
+                   dict(EBIC_SPLIT="0"), dict(EBIC_SPLIT="1"), dict(EBIC_SPLIT="1", EBIC_NO_COLLAPSE="1"),
+                   dict(EBIC_SPLIT="1", EBIC_PACK="0"), dict(EBIC_SPLIT="1", EBIC_GRID="1000"),
+                   dict(EBIC_SPLIT="1", EBIC_GRID="3")])
 
 
 @contextmanager
@@ -200,8 +204,36 @@ def test_v2_column_runs_vs_oracle(cfg):
                         assert (got == want).all(), (rows, name, eps)
 
 
-PACK_CONFIGS = [dict(), dict(EBIC_COMPACT="1"), dict(EBIC_COMPACT="0"), dict(EBIC_GRID="7"),
-                dict(EBIC_COMPACT="1", EBIC_GRID="7"), dict(EBIC_STAGES="1"), dict(EBIC_V2_NP="4")]
+@pytest.mark.parametrize("grid", ["", "40", "148", "4000"])
+def test_split_kernel_partition_vs_oracle(grid):
+    """K1s splits series x row tiles by length-weighted units: series split
+    over 2+ CTAs (partial sums, arrival counters), CTA ranges shorter than one
+    series (some CTAs in a series' span hold none of its tiles), few CTAs with
+    many series per CTA, length-0/1 series, many more CTAs than work."""
+    rng = np.random.default_rng(44)
+    cfg = dict(EBIC_SPLIT="1", **({"EBIC_GRID": grid} if grid else {}))
+    with env(**cfg):
+        for rows, n_cols in ((40, 30), (960, 100), (5000, 400)):
+            v = np.round(rng.standard_normal((rows, n_cols)), 1)
+            series = random_population(rng, n_cols, 300, max_len=20) + [[], [3], [7, 7], list(range(n_cols))[:25]]
+            rng.shuffle(series)
+            pop = cbf(series)
+            with eb.Evaluator(v) as ev:
+                for eps in (0.0, 1e-9, 0.05):
+                    for rep in range(2):  # the accumulators must come back zeroed
+                        got = ev.count_matches(pop, eps)
+                        want = port.count_matches(v, pop.offsets, pop.col_indices, eps)
+                        assert (got == want).all(), (grid, rows, eps, rep)
+                    f, c = ev.evaluate_population(pop, eb.FitnessParams(max(4, rows // 50)), eps, return_counts=True)
+                    _, wf = port.evaluate_population(v, pop.offsets, pop.col_indices, max(4, rows // 50), eps)
+                    assert bits_equal(f, wf)
+                    assert ev.info().kernel == 3
+
+
+PACK_CONFIGS = [dict(), dict(EBIC_SPLIT="0"), dict(EBIC_COMPACT="1"), dict(EBIC_COMPACT="0", EBIC_SPLIT="0"),
+                dict(EBIC_GRID="7", EBIC_SPLIT="0"), dict(EBIC_COMPACT="1", EBIC_GRID="7"), dict(EBIC_STAGES="1"),
+                dict(EBIC_V2_NP="4", EBIC_SPLIT="0"), dict(EBIC_SPLIT="1", EBIC_GRID="1000"),
+                dict(EBIC_SPLIT="1", EBIC_GRID="5")]
 
 
 @pytest.mark.parametrize("cfg", PACK_CONFIGS, ids=lambda d: "-".join(f"{k}={v}" for k, v in d.items()) or "default")
@@ -232,7 +264,8 @@ def test_v2_packed_ranks_vs_oracle(cfg):
                 assert bits_equal(f, wf)
 
 
-@pytest.mark.parametrize("cfg", [dict(), dict(EBIC_COMPACT="1"), dict(EBIC_KERNEL="1")], ids=str)
+@pytest.mark.parametrize("cfg", [dict(EBIC_SPLIT="0"), dict(EBIC_SPLIT="1"), dict(EBIC_COMPACT="1"),
+                                 dict(EBIC_KERNEL="1")], ids=str)
 def test_host_cbf_staging_without_cta0(cfg):
     """Host-buffer calls: the population is copied to the device by CTA 0 and
     published with a flag.  EBIC_DEBUG_MODE=4 suppresses the flag, so every
