@@ -135,9 +135,11 @@ class ClockSampler:
 
 
 # bytes per matrix cell of the layout the count kernel streams (ebic_ctx_info.layout)
-# (4, 5: one plane packed three rows per 32-bit word, 128 B per 96 rows)
-LAYOUT_CELL_BYTES = {0: 8, 1: 2, 2: 4, 3: 2, 4: 4 / 3, 5: 4 / 3}
-LAYOUT_NAMES = {0: "fp64", 1: "rank16x1", 2: "rank16x2", 3: "rank16x1c", 4: "rank10x3", 5: "rank10x3c"}
+# (4, 5: one plane packed three rows per 32-bit word, 128 B per 96 rows;
+#  6, 7: five rows per 64-bit word, 128 B per 80 rows)
+LAYOUT_CELL_BYTES = {0: 8, 1: 2, 2: 4, 3: 2, 4: 4 / 3, 5: 4 / 3, 6: 1.6, 7: 1.6}
+LAYOUT_NAMES = {0: "fp64", 1: "rank16x1", 2: "rank16x2", 3: "rank16x1c", 4: "rank10x3", 5: "rank10x3c",
+                6: "rank12x5", 7: "rank12x5c"}
 
 
 def algorithmic_bytes(rows: int, off: np.ndarray, cols: np.ndarray, cell_bytes: int) -> int:

@@ -77,7 +77,8 @@ typedef struct ebic_ctx_info {
     int sm_count;         /* SMs of shard 0's device */
     int layout;           /* last count launch: 0 fp64 tile, 1/2 = exact rank tile (planes),
                              3 = one-plane collapsed rank tile (eps > 0), 4/5 = the one-plane
-                             tile (strict / collapsed) packed three rows per 32-bit word */
+                             tile (strict / collapsed) packed three rows per 32-bit word,
+                             6/7 = five rows per 64-bit word */
     int consumer_warps;   /* count-kernel consumer warps per CTA */
     int kernel;           /* last count launch: 1 = v1 tile or direct kernel, 2 = K1v2
                              (row tiles per CTA), 3 = K1s (series per CTA) */

@@ -198,7 +198,7 @@ struct RankLayout {
     // fits 9 bits (n_cols <= kPack10MaxCols); K1v2 streams this one
     uint32_t* d10 = nullptr;
     size_t d10_bytes = 0;
-    bool packed = false;
+    int packed = 0;  // 0 none, 3 = 10-bit fields (RankWalker<3>), 4 = 12-bit fields (RankWalker<4>)
     // rows the collapsed layout cannot represent (evaluated exactly in fp64)
     unsigned long long* d_row_excl = nullptr;  // bitmask, ceil(ld / 64) words
     uint32_t* d_excl_rows = nullptr;
@@ -593,8 +593,8 @@ CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int
             c.v2 = 1;
             c.layout = rank_planes;
             c.slice = 128;
-            c.rpg = rank_planes == 3 ? 96 : rank_planes == 2 ? 32 : 64;
-            c.rpl = rank_planes == 3 ? 12 : rank_planes == 2 ? 4 : 8;
+            c.rpg = rank_planes == 4 ? 80 : rank_planes == 3 ? 96 : rank_planes == 2 ? 32 : 64;
+            c.rpl = rank_planes == 4 ? 10 : rank_planes == 3 ? 12 : rank_planes == 2 ? 4 : 8;
             c.ncw = 24;
             c.spg = 2;
             c.stages = kn.stages;  // 0: as many as fit (<= 4)
@@ -603,7 +603,7 @@ CountConfig choose_config(const Shard& s, size_t n_cols, size_t P, size_t L, int
             if ((tiles / std::max(1, std::min<int>((int)tiles, s.sm_count)) + 2) * c.rpl <= 0xffff) return c;
         }
     }
-    if (rank_planes == 3) rank_planes = 1;  // v1: the 16-bit plane
+    if (rank_planes >= 3) rank_planes = 1;  // v1: the 16-bit plane
     if (rank_planes) {
         const int want_slice = kn.slice;
         for (int min_stages : {3, 2}) {
@@ -770,7 +770,8 @@ void launch_tma(const CountConfig& c, bool e0, const CUtensorMap& tm, const Coun
 }
 
 constexpr size_t kRankMaxCols = 2048;  // 2C keys sorted in shared memory per row
-constexpr size_t kPack10MaxCols = 510;  // ranks 1..510 + the NaN sentinel in 9 bits
+constexpr size_t kPack10MaxCols = 510;   // ranks 1..510 + the NaN sentinel in 9 bits
+constexpr size_t kPack12MaxCols = 2046;  // ranks 1..2046 + the NaN sentinel in 11 bits
 constexpr double kSplitMaxL2Bytes = 4e6;  // K1s while rows x sum(len) x b stays below this (measured crossover: C1 1.6 MB K1s faster, C3 17 MB K1v2 faster)
 
 uint64_t eps_key(double eps) {
@@ -876,9 +877,12 @@ RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
         rl.planes = 2;
         launch_rank_build<2, false>(s, n_cols, eps, rl.d, nullptr);
     }
-    rl.packed = false;
-    if (rl.planes == 1 && n_cols <= kPack10MaxCols && s.knobs.pack && s.knobs.kernel == 2) {
-        const uint32_t tiles = (uint32_t)((s.rows + 95) / 96);
+    rl.packed = 0;
+    if (rl.planes == 1 && n_cols <= kPack12MaxCols && s.knobs.pack && s.knobs.kernel == 2) {
+        // three rows per 32-bit word while ranks fit 9 bits, else five per 64-bit word
+        const bool ten = n_cols <= kPack10MaxCols && s.knobs.pack != 12;
+        const uint32_t rpt = ten ? 96 : 80;
+        const uint32_t tiles = (uint32_t)((s.rows + rpt - 1) / rpt);
         const size_t bytes = size_t(tiles) * n_cols * 128;
         if (rl.d10_bytes < bytes) {
             if (rl.d10) CK(cudaFree(rl.d10));
@@ -886,10 +890,14 @@ RankLayout* ensure_ranks(Shard& s, size_t n_cols, double eps) {
             CK(cudaMalloc(&rl.d10, bytes));
             rl.d10_bytes = bytes;
         }
-        rank_pack10_kernel<<<s.sm_count * 8, 256, 0, s.stream>>>(rl.d, (uint32_t)s.ld, (uint32_t)n_cols, tiles,
-                                                               rl.d10);
+        if (ten)
+            rank_pack10_kernel<<<s.sm_count * 8, 256, 0, s.stream>>>(rl.d, (uint32_t)s.ld, (uint32_t)n_cols, tiles,
+                                                                   rl.d10);
+        else
+            rank_pack12_kernel<<<s.sm_count * 8, 256, 0, s.stream>>>(
+                rl.d, (uint32_t)s.ld, (uint32_t)n_cols, tiles, reinterpret_cast<unsigned long long*>(rl.d10));
         CK(cudaGetLastError());
-        rl.packed = true;
+        rl.packed = ten ? 3 : 4;
     }
     CK(cudaStreamSynchronize(s.stream));
     rl.ok = true;
@@ -1002,14 +1010,14 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
     }
     const bool e0 = (eps == 0.0);
     RankLayout* rl = ensure_ranks(s, ctx.n_cols, eps);
-    const int planes = rl ? (rl->packed ? 3 : rl->planes) : 0;
+    const int planes = rl ? (rl->packed ? rl->packed : rl->planes) : 0;
     if (!(s.memo_P == P && s.memo_L == L && s.memo_planes == planes)) {
         s.memo_cfg = choose_config(s, ctx.n_cols, P, L, planes);
         s.memo_P = P, s.memo_L = L, s.memo_planes = planes;
     }
     const CountConfig c = s.memo_cfg;
     if (c.v2) {
-        p.ranks = c.layout == 3 ? reinterpret_cast<const unsigned char*>(rl->d10)
+        p.ranks = c.layout >= 3 ? reinterpret_cast<const unsigned char*>(rl->d10)
                                 : reinterpret_cast<const unsigned char*>(rl->d);
         p.stages = (uint32_t)c.stages;
         p.n_tiles = (uint32_t)((s.rows + c.rpg - 1) / c.rpg);
@@ -1040,7 +1048,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         // whole series over all rows, reading its columns' slices through L2
         // (rows x sum(len) x b bytes) -- no length sort, no cross-CTA sum
         const int sgrid = s.knobs.grid > 0 ? s.knobs.grid : 2 * s.sm_count;
-        const double cell = c.layout == 3 ? 4.0 / 3.0 : c.layout == 2 ? 4.0 : 2.0;
+        const double cell = c.layout == 4 ? 1.6 : c.layout == 3 ? 4.0 / 3.0 : c.layout == 2 ? 4.0 : 2.0;
         const bool use_s = !xacc && L <= size_t(kSMaxMine) * (size_t)sgrid &&
                            (s.knobs.split == 1 ||
                             (s.knobs.split < 0 && !long_launch && double(s.rows) * L * cell <= kSplitMaxL2Bytes));
@@ -1050,9 +1058,12 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         s.last_kernel = use_s ? 3 : 2;
         ensure_partial(s, P, use_s ? sgrid : grid, use_s ? 3 : (int)p.reduce_striped);
         p.partial = s.d_partial;
-        if (c.layout == 3) {
-            // packed fields: + 0x1ff (strict <) or + 0x200 (<=, collapsed) per field
-            p.rank_k = rl->collapsed ? 0x20080200u : 0x1ff7fdffu;
+        if (c.layout >= 3) {
+            // packed fields: + 0x1ff (strict <) or + 0x200 (<=, collapsed) per
+            // 10-bit field; the 12-bit walker derives its 64-bit constant from
+            // the 16-bit codes
+            p.rank_k = c.layout == 4 ? (rl->collapsed ? 0x80008000u : 0x7fff7fffu)
+                                     : (rl->collapsed ? 0x20080200u : 0x1ff7fdffu);
             p.row_excl = rl->d_row_excl;
             p.excl_rows = rl->d_excl_rows;
             p.excl_vals = rl->d_excl_vals;
@@ -1067,14 +1078,15 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
             p.rank_k = 0x7fff7fffu;
         }
         if (use_s) {
-            const void* fs = c.layout == 3   ? reinterpret_cast<const void*>(count_s_kernel<3>)
+            const void* fs = c.layout == 4   ? reinterpret_cast<const void*>(count_s_kernel<4>)
+                             : c.layout == 3 ? reinterpret_cast<const void*>(count_s_kernel<3>)
                              : c.layout == 2 ? reinterpret_cast<const void*>(count_s_kernel<2>)
                                              : reinterpret_cast<const void*>(count_s_kernel<1>);
             s.last_cfg.ncw = kSThreads / 32;
             s.last_cfg.stages = 0;
             void* args[1] = {const_cast<CountParams*>(&p)};
             const size_t ssmem = (P + 1 + L) * sizeof(uint32_t);  // offsets + my column lists (<= L)
-            static std::atomic<int> s_smem_set[3][64] = {};
+            static std::atomic<int> s_smem_set[4][64] = {};
             std::atomic<int>& sflag = s_smem_set[c.layout - 1][s.device & 63];
             if (ssmem > 48 * 1024 && sflag.load(std::memory_order_acquire) < (int)ssmem) {
                 CK(cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
@@ -1090,7 +1102,10 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         const int np = s.knobs.v2_np == 4 ? 4 : 8;
         const int ncw = np == 8 ? 20 : 24;
         const void* fn;
-        if (c.layout == 3)
+        if (c.layout == 4)
+            fn = np == 8 ? reinterpret_cast<const void*>(count_v2_kernel<4, 20, 8>)
+                         : reinterpret_cast<const void*>(count_v2_kernel<4, 24, 4>);
+        else if (c.layout == 3)
             fn = np == 8 ? reinterpret_cast<const void*>(count_v2_kernel<3, 20, 8>)
                          : reinterpret_cast<const void*>(count_v2_kernel<3, 24, 4>);
         else if (c.layout == 2)
@@ -1099,7 +1114,7 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         else
             fn = np == 8 ? reinterpret_cast<const void*>(count_v2_kernel<1, 20, 8>)
                          : reinterpret_cast<const void*>(count_v2_kernel<1, 24, 4>);
-        static std::atomic<int> v2_smem_set[3][2][64] = {};
+        static std::atomic<int> v2_smem_set[4][2][64] = {};
         std::atomic<int>& flag = v2_smem_set[c.layout - 1][np == 8 ? 1 : 0][s.device & 63];
         if (flag.load(std::memory_order_acquire) < (int)smem) {
             CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1702,6 +1717,7 @@ int ebic_ctx_get_info(const ebic_ctx* ctx, ebic_ctx_info* info) {
         info->layout = s.last_cfg.layout;
         if (s.last_cfg.layout == 1 && s.last_collapsed) info->layout = 3;
         if (s.last_cfg.layout == 3) info->layout = s.last_collapsed ? 5 : 4;  // packed 10-bit fields
+        if (s.last_cfg.layout == 4) info->layout = s.last_collapsed ? 7 : 6;  // packed 12-bit fields
         info->consumer_warps = s.last_cfg.ncw == 32 ? 31 : s.last_cfg.ncw;
         info->kernel = s.last_kernel;
     });

@@ -848,16 +848,25 @@ struct F64Walker {
 //     (each field of the sum is in [0, 0x3fe]: no carry between fields).
 //     A lane owns 12 consecutive rows (one LDS.128), a tile 96 rows: a third
 //     fewer bytes per row to stream, stage and test than one 16-bit plane.
-// Tile: 128 bytes per column (32 rows x 2 planes, 64 rows x 1 plane, or 96
-// packed rows).
+//   PLANES == 4 (K1v2/K1s; one plane, ranks up to 2046 distinct values):
+//     five rows per 64-bit word in 12-bit fields (r | 0x800, row 5w + f of an
+//     80-row tile in bits 12f..12f+11 of word w), the test one 64-bit add
+//     (IADD3 + IADD3.X) and AND per two words:
+//         ok &= cur' - prev' + 0x07ff7ff7ff7ff7ff   (or + 0x0800800800800800)
+//     a lane owns 10 rows (two words), a tile 80 rows: a fifth fewer bytes
+//     per row than one 16-bit plane for matrices too wide for PLANES == 3.
+// Tile: 128 bytes per column (32 rows x 2 planes, 64 rows x 1 plane, or 96 /
+// 80 packed rows).
 // ---------------------------------------------------------------------------
 template <int PLANES, int SLICE, int SPG = 2>
 struct RankWalker {
     static_assert(SLICE == 64 || SLICE == 128, "column slice of 64 or 128 bytes");
-    static_assert(PLANES != 3 || SLICE == 128, "packed ranks: 128-byte slices");
+    static_assert(PLANES < 3 || SLICE == 128, "packed ranks: 128-byte slices");
     static constexpr bool kPacked = PLANES == 3;
-    static constexpr int kRowsPerLane = kPacked ? 12 : PLANES == 2 ? 4 : 8;
-    static constexpr int kRowsPerTile = kPacked ? 96 : SLICE / (2 * PLANES);
+    static constexpr bool kPacked64 = PLANES == 4;
+    static constexpr int kRowsPerLane = kPacked ? 12 : kPacked64 ? 10 : PLANES == 2 ? 4 : 8;
+    static constexpr int kRowsPerTile = kPacked ? 96 : kPacked64 ? 80 : SLICE / (2 * PLANES);
+    static constexpr uint64_t kStrict64 = 0x07ff7ff7ff7ff7ffull, kCollapsed64 = 0x0800800800800800ull;
     static constexpr int kLaneBytes = 16;
     static constexpr int kColBytes = SLICE;
     static constexpr int kShift = SLICE == 128 ? 7 : 6;
@@ -866,7 +875,7 @@ struct RankWalker {
     // one column's rows, [block][column][64 u16]; a 64-byte slice is half a block.
     static constexpr bool kTileMajor = true;
     static constexpr int kSlicesPerBlock = 128 / SLICE;
-    static constexpr int kWords = kPacked ? 4 : kRowsPerLane / 2;  // ok words per lane
+    static constexpr int kWords = (kPacked || kPacked64) ? 4 : kRowsPerLane / 2;  // ok words per lane
     static constexpr int kSeriesPerGroup = SPG;               // independent walks per group
     static constexpr int kFieldBits = 32 / SPG;               // packed per-series counts
     static_assert(SPG == 2 || SPG == 4, "2 or 4 series per lane group");
@@ -874,14 +883,28 @@ struct RankWalker {
     // tally() folds word k down by k bits (rows land on bits 15-k / 31-k)
     // and counts once; `m` is the lane's valid-row mask in that folded form.
     struct Mask {
-        uint32_t m;  // folded valid-row mask
-        uint32_t k;  // per-pair constant: 0x7fff7fff (strict <) or 0x80008000 (<=, collapsed)
+        uint32_t m;     // folded valid-row mask
+        uint32_t k;     // per-pair constant: 0x7fff7fff (strict <) or 0x80008000 (<=, collapsed)
+        uint32_t m_hi;  // PLANES == 4: high half of the 64-bit folded mask
     };
     // excl: bit j set = the lane's row j is excluded (fixed up separately).
     __device__ __forceinline__ static Mask valid(uint32_t row0, uint32_t n_rows, uint32_t excl,
                                                  uint32_t kconst) {
         Mask v;
         v.m = 0;
+        v.m_hi = 0;
+        if constexpr (kPacked64) {  // row 5w + f: bit 11 + 12 f of 64-bit word w, folded down by w
+            uint64_t m = 0;
+#pragma unroll
+            for (int w = 0; w < 2; ++w)
+#pragma unroll
+                for (int f = 0; f < 5; ++f)
+                    if (row0 + 5 * w + f < n_rows && !((excl >> (5 * w + f)) & 1u)) m |= (1ull << (11 + 12 * f)) >> w;
+            v.m = static_cast<uint32_t>(m);
+            v.m_hi = static_cast<uint32_t>(m >> 32);
+            v.k = kconst;
+            return v;
+        }
         if constexpr (kPacked) {  // row 3k + f: bit 9 + 10 f of word k, folded down by k
 #pragma unroll
             for (int k = 0; k < 4; ++k)
@@ -924,7 +947,15 @@ struct RankWalker {
     // K = 0x80008000 tests r(prev) <= r(cur) (collapsed eps > 0 layout).
     __device__ __forceinline__ static void step(uint32_t* ok, const uint4& prev, const uint4& cur,
                                                 uint32_t K) {
-        if (PLANES == 2) {
+        if constexpr (kPacked64) {
+            const uint64_t K64 = (K & 1u) ? kStrict64 : kCollapsed64;  // from the 16-bit constants
+            const uint64_t t0 = ((uint64_t(cur.y) << 32) | cur.x) - ((uint64_t(prev.y) << 32) | prev.x) + K64;
+            const uint64_t t1 = ((uint64_t(cur.w) << 32) | cur.z) - ((uint64_t(prev.w) << 32) | prev.z) + K64;
+            ok[0] &= static_cast<uint32_t>(t0);
+            ok[1] &= static_cast<uint32_t>(t0 >> 32);
+            ok[2] &= static_cast<uint32_t>(t1);
+            ok[3] &= static_cast<uint32_t>(t1 >> 32);
+        } else if (PLANES == 2) {
             ok[0] &= cur.z - prev.x + 0x7fff7fffu;
             ok[1] &= cur.w - prev.y + 0x7fff7fffu;
         } else {
@@ -935,6 +966,11 @@ struct RankWalker {
         }
     }
     __device__ __forceinline__ static uint32_t tally(const uint32_t* ok, const Mask& vm) {
+        if constexpr (kPacked64) {  // result bits 11 + 12 f of each 64-bit word
+            const uint64_t a = (uint64_t(ok[1]) << 32) | ok[0], b = (uint64_t(ok[3]) << 32) | ok[2];
+            const uint64_t f = (a & kCollapsed64) | ((b & kCollapsed64) >> 1);
+            return __popc(static_cast<uint32_t>(f) & vm.m) + __popc(static_cast<uint32_t>(f >> 32) & vm.m_hi);
+        }
         constexpr uint32_t kRes = kPacked ? 0x20080200u : 0x80008000u;  // result bits of an ok word
         uint32_t f = ok[0] & kRes;
 #pragma unroll
@@ -1512,6 +1548,31 @@ __global__ void rank_pack10_kernel(const uint16_t* __restrict__ in, uint32_t in_
                 v = u == 0xffffu ? 0x3ffu : (0x200u | (u & 0x1ffu));
             }
             x |= v << (10 * f);
+        }
+        out[i] = x;
+    }
+}
+
+// The same into RankWalker<4>: [tile][column][16 u64], 80 rows per tile, row
+// 5w + f in bits 12f..12f+11 of word w; 0x800 | r (r <= 0x7fe), NaN 0xfff.
+__global__ void rank_pack12_kernel(const uint16_t* __restrict__ in, uint32_t in_rows, uint32_t n_cols,
+                                   uint32_t n_tiles, unsigned long long* __restrict__ out) {
+    const size_t n = size_t(n_tiles) * n_cols * 16;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const uint32_t w = static_cast<uint32_t>(i & 15);
+        const size_t tc = i >> 4;
+        const uint32_t c = static_cast<uint32_t>(tc % n_cols);
+        const uint32_t t = static_cast<uint32_t>(tc / n_cols);
+        unsigned long long x = 0;
+#pragma unroll
+        for (int f = 0; f < 5; ++f) {
+            const uint32_t r = t * 80 + 5 * w + f;
+            unsigned long long v = 0x800u;
+            if (r < in_rows) {
+                const uint32_t u = in[(size_t(r / 64) * n_cols + c) * 64 + (r % 64)];
+                v = u == 0xffffu ? 0xfffu : (0x800u | (u & 0x7ffu));
+            }
+            x |= v << (12 * f);
         }
         out[i] = x;
     }

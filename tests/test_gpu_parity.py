@@ -35,7 +35,10 @@ KERNEL_CONFIGS = ([dict(), dict(EBIC_NCW="16"), dict(EBIC_NCW="24"), dict(EBIC_N
                    # K1s (series per CTA; default for short launches) against K1v2, and its shapes
                    dict(EBIC_SPLIT="0"), dict(EBIC_SPLIT="1"), dict(EBIC_SPLIT="1", EBIC_NO_COLLAPSE="1"),
                    dict(EBIC_SPLIT="1", EBIC_PACK="0"), dict(EBIC_SPLIT="1", EBIC_GRID="1000"),
-                   dict(EBIC_SPLIT="1", EBIC_GRID="3")])
+                   dict(EBIC_SPLIT="1", EBIC_GRID="3"),
+                   # five rows per 64-bit word (default above 510 columns) also on narrow matrices
+                   dict(EBIC_PACK="12"), dict(EBIC_PACK="12", EBIC_SPLIT="0", EBIC_COMPACT="1"),
+                   dict(EBIC_PACK="12", EBIC_SPLIT="1")])
 
 
 @contextmanager
@@ -233,7 +236,8 @@ def test_split_kernel_partition_vs_oracle(grid):
 PACK_CONFIGS = [dict(), dict(EBIC_SPLIT="0"), dict(EBIC_COMPACT="1"), dict(EBIC_COMPACT="0", EBIC_SPLIT="0"),
                 dict(EBIC_GRID="7", EBIC_SPLIT="0"), dict(EBIC_COMPACT="1", EBIC_GRID="7"), dict(EBIC_STAGES="1"),
                 dict(EBIC_V2_NP="4", EBIC_SPLIT="0"), dict(EBIC_SPLIT="1", EBIC_GRID="1000"),
-                dict(EBIC_SPLIT="1", EBIC_GRID="5")]
+                dict(EBIC_SPLIT="1", EBIC_GRID="5"), dict(EBIC_PACK="12", EBIC_SPLIT="0"),
+                dict(EBIC_PACK="12", EBIC_SPLIT="1"), dict(EBIC_PACK="12", EBIC_COMPACT="1", EBIC_SPLIT="0")]
 
 
 @pytest.mark.parametrize("cfg", PACK_CONFIGS, ids=lambda d: "-".join(f"{k}={v}" for k, v in d.items()) or "default")
@@ -258,7 +262,7 @@ def test_v2_packed_ranks_vs_oracle(cfg):
                     want = port.count_matches(v, pop.offsets, pop.col_indices, eps)
                     assert (got == want).all(), (rows, n_cols, eps)
                     if eps == 0.0:
-                        assert ev.info().layout == 4, ev.info().layout
+                        assert ev.info().layout == (6 if os.environ.get("EBIC_PACK") == "12" else 4), ev.info().layout
                 f = ev.evaluate_population(pop, eb.FitnessParams(max(4, rows // 50)), 1e-6)
                 _, wf = port.evaluate_population(v, pop.offsets, pop.col_indices, max(4, rows // 50), 1e-6)
                 assert bits_equal(f, wf)
