@@ -17,7 +17,7 @@ PKG = CSRC.parent
 REPO = PKG.parent
 LIB = PKG / "libebic_b200.so"
 SOURCES = [CSRC / "ebic_b200.cu", CSRC / "synth.cpp", CSRC / "toprank.cpp"]
-DEPS = SOURCES + [CSRC / "kernels.cuh", REPO / "include" / "ebic_b200.h"]
+DEPS = SOURCES + sorted(CSRC.glob("*.cuh")) + [REPO / "include" / "ebic_b200.h"]
 E2E = PKG / "ebic_e2e_driver"
 E2E_SRC = CSRC / "e2e_driver.cu"
 
@@ -27,7 +27,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # (bit-exact parity with the reference's x86-64 SSE2 arithmetic).
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--expt-relaxed-constexpr",
          "-Xcompiler", "-fPIC,-O2,-ffp-contract=off,-fvisibility=hidden",
-         "-Xptxas", "-warn-spills"]
+         "-Xptxas", "-warn-spills"] + os.environ.get("EBIC_NVCC_EXTRA", "").split()  # (experiments only)
 
 
 def needs_build() -> bool:

@@ -35,6 +35,15 @@ namespace ebic_b200 {
 constexpr int kV2MaxCols = 2048;    // bitmap of 64 words
 constexpr int kV2Chunk = 8;         // slots per warp iteration (4 groups x 2 series)
 constexpr int kV2MaxStages = 4;
+#ifndef EBIC_V2_MAX_UNROLL
+#define EBIC_V2_MAX_UNROLL 8
+#endif
+// longest series length with a fully unrolled chunk walk (longer: per-slot
+// loop).  Fewer unrolled variants keep the walk's code in the instruction
+// cache: C5 steady state 76.7 us at 12, 74.7 at 8, 74.1 at 6, 77.6 at 4
+// (profiles/r02_kernel_variants.log); C4 unchanged.
+constexpr uint32_t kV2MaxUnroll = EBIC_V2_MAX_UNROLL;
+static_assert(kV2MaxUnroll >= 3 && kV2MaxUnroll <= 12, "unrolled chunk lengths 2..3+");
 constexpr uint32_t kV2ExclItems = 64;  // per-CTA items whose excl words are preloaded
 
 // Byte offsets of the persistent work list inside the dynamic window.
@@ -322,7 +331,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
         for (int k = 0; k < 2; ++k) {
             const int b = tid + 32 * k;
             uint32_t c = orig[b];
-            if (b >= 2 && b <= 12) c = (c + CHUNK - 1) / CHUNK * CHUNK;
+            if (b >= 2 && b <= kV2MaxUnroll) c = (c + CHUNK - 1) / CHUNK * CHUNK;
             if (b == 1) c = (orig[0] + orig[1] + CHUNK - 1) / CHUNK * CHUNK - orig[0];
             w.hist[b] = c;
             w.hpad[b] = b < kLenBuckets - 1 ? c * pad4(b) : 0u;
@@ -366,7 +375,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
                 // stride pad4(length)) and the length is unrolled (2..12); else
                 // 0 (per-slot path).  Bucket b ends where bucket b + 1 starts.
                 const uint32_t end = w.hist[bkt + 1];
-                const bool uni = g + CHUNK <= end && len >= 2 && len <= 12;
+                const bool uni = g + CHUNK <= end && len >= 2 && len <= kV2MaxUnroll;
                 reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = uni ? ((st << 8) | len) : 0u;
             }
             if (compact) {
@@ -406,7 +415,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
             else reinterpret_cast<uint4*>(w.pcols)[st / 4 + q] = make_uint4(0u, 0u, 0u, 0u);
         }
         if (g % CHUNK == 0)
-            reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = (b >= 2 && b <= 12) ? ((st << 8) | b) : 0u;
+            reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = (b >= 2 && b <= kV2MaxUnroll) ? ((st << 8) | b) : 0u;
     }
     if (tid == 0) reinterpret_cast<uint32_t*>(smem + v.misc)[3] = pslots;
     if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 601 + 1] = global_ns();
@@ -498,18 +507,21 @@ __device__ __forceinline__ uint32_t v2_count2(uint32_t base, const uint32_t* pc,
 template <class W>
 __device__ __forceinline__ uint32_t v2_count_uniform(uint32_t L, uint32_t base, const uint32_t* pc, uint32_t stride,
                                                      const typename W::Mask& vm) {
+    // (lengths above kV2MaxUnroll never get a uniform descriptor; their cases
+    // alias the longest instantiation so no extra walk code is generated)
+    constexpr uint32_t M = kV2MaxUnroll;
     switch (L) {
         case 2: return v2_count2<W, 2>(base, pc, stride, vm);
         case 3: return v2_count2<W, 3>(base, pc, stride, vm);
-        case 4: return v2_count2<W, 4>(base, pc, stride, vm);
-        case 5: return v2_count2<W, 5>(base, pc, stride, vm);
-        case 6: return v2_count2<W, 6>(base, pc, stride, vm);
-        case 7: return v2_count2<W, 7>(base, pc, stride, vm);
-        case 8: return v2_count2<W, 8>(base, pc, stride, vm);
-        case 9: return v2_count2<W, 9>(base, pc, stride, vm);
-        case 10: return v2_count2<W, 10>(base, pc, stride, vm);
-        case 11: return v2_count2<W, 11>(base, pc, stride, vm);
-        default: return v2_count2<W, 12>(base, pc, stride, vm);
+        case 4: return v2_count2<W, (4 < M ? 4 : M)>(base, pc, stride, vm);
+        case 5: return v2_count2<W, (5 < M ? 5 : M)>(base, pc, stride, vm);
+        case 6: return v2_count2<W, (6 < M ? 6 : M)>(base, pc, stride, vm);
+        case 7: return v2_count2<W, (7 < M ? 7 : M)>(base, pc, stride, vm);
+        case 8: return v2_count2<W, (8 < M ? 8 : M)>(base, pc, stride, vm);
+        case 9: return v2_count2<W, (9 < M ? 9 : M)>(base, pc, stride, vm);
+        case 10: return v2_count2<W, (10 < M ? 10 : M)>(base, pc, stride, vm);
+        case 11: return v2_count2<W, (11 < M ? 11 : M)>(base, pc, stride, vm);
+        default: return v2_count2<W, M>(base, pc, stride, vm);
     }
 }
 
