@@ -16,7 +16,7 @@
 //    conflicts) fits twice or more in shared memory where the full tile
 //    fitted only with 32-row tiles.  The ring depth follows U at run time.
 //  * Walk.  Slots are length-sorted; a chunk (8 consecutive slots, 4 lane
-//    groups x 2 series) of one length <= 12 is described by one word
+//    groups x 2 series) of one length <= kV2MaxUnroll is described by one word
 //    (length, first list entry), so the walk loads no per-slot metadata:
 //    slot lists are consecutive with stride pad4(length).  Chunks are
 //    assigned to warps statically (longest first, rotated every tile), and
@@ -64,7 +64,7 @@ struct V2Layout {
 
 __host__ __device__ inline uint32_t v2_max_runs(uint32_t n_cols) { return (n_cols + 1) / 2 + 1; }
 
-// Length buckets 2..12 are padded to whole chunks with dummy slots (so every
+// Length buckets 2..kV2MaxUnroll are padded to whole chunks with dummy slots (so every
 // chunk of those lengths is uniform), bucket 1 so that bucket 2 starts on a
 // chunk: at most kV2Pad extra slots.
 constexpr uint32_t kV2Pad = 7 * 12;
@@ -372,7 +372,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
             if (g % CHUNK == 0) {
                 // chunk descriptor: (first list entry << 8) | length when the
                 // whole chunk lies in this length's bucket (lists consecutive,
-                // stride pad4(length)) and the length is unrolled (2..12); else
+                // stride pad4(length)) and the length is unrolled (2..kV2MaxUnroll); else
                 // 0 (per-slot path).  Bucket b ends where bucket b + 1 starts.
                 const uint32_t end = w.hist[bkt + 1];
                 const bool uni = g + CHUNK <= end && len >= 2 && len <= kV2MaxUnroll;
