@@ -319,7 +319,7 @@ def test_wide_matrix_direct_path():
 
 
 @pytest.mark.parametrize("xshard", ["1", "0"])
-@pytest.mark.parametrize("devices,name", [([0, 0, 0], "c3"), ([0, 0], "c4"), ([0] * 5, "c1e")])
+@pytest.mark.parametrize("devices,name", [([0, 0, 0], "c3"), ([0, 0], "c4"), ([0] * 5, "c1e"), ([0, 0], "c5")])
 def test_row_shards_on_one_device_are_partition_invariant(xshard, devices, name):
     """Several 64-row-aligned shards on one GPU.  EBIC_XSHARD=1: every shard's
     kernel adds its totals into one accumulator and the last to finish writes
