@@ -48,7 +48,9 @@ extern "C" {
 #pragma GCC visibility push(default)
 #endif
 
-#define EBIC_B200_ABI_VERSION 1
+/* 2: ebic_ctx_info gained `kernel` (appended); callers built against version 1
+ * pass a smaller struct to ebic_ctx_get_info and must be rebuilt. */
+#define EBIC_B200_ABI_VERSION 2
 
 typedef enum ebic_status {
     EBIC_OK = 0,

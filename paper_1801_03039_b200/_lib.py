@@ -10,6 +10,7 @@ import ctypes as C
 import os
 from pathlib import Path
 
+ABI_VERSION = 2  # EBIC_B200_ABI_VERSION of include/ebic_b200.h
 LIB_PATH = Path(os.environ.get("EBIC_B200_LIB", Path(__file__).resolve().parent / "libebic_b200.so"))
 
 u8p = C.POINTER(C.c_uint8)
@@ -91,6 +92,9 @@ def _load() -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.ebic_abi_version() != ABI_VERSION:  # a stale build: struct layouts differ
+        raise ImportError(f"{LIB_PATH} has ABI version {lib.ebic_abi_version()}, this binding "
+                          f"expects {ABI_VERSION}: rebuild it")
     return lib
 
 

@@ -42,7 +42,7 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version():
-    assert _lib.lib.ebic_abi_version() == 1
+    assert _lib.lib.ebic_abi_version() == 2
 
 
 def test_no_device_fails_loudly():
