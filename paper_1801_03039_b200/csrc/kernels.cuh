@@ -948,13 +948,26 @@ struct RankWalker {
     __device__ __forceinline__ static void step(uint32_t* ok, const uint4& prev, const uint4& cur,
                                                 uint32_t K) {
         if constexpr (kPacked64) {
+            // cur - prev + K per 64-bit word as two carry chains (4 integer
+            // adds; the compiler's own lowering negates first and takes 5)
             const uint64_t K64 = (K & 1u) ? kStrict64 : kCollapsed64;  // from the 16-bit constants
-            const uint64_t t0 = ((uint64_t(cur.y) << 32) | cur.x) - ((uint64_t(prev.y) << 32) | prev.x) + K64;
-            const uint64_t t1 = ((uint64_t(cur.w) << 32) | cur.z) - ((uint64_t(prev.w) << 32) | prev.z) + K64;
-            ok[0] &= static_cast<uint32_t>(t0);
-            ok[1] &= static_cast<uint32_t>(t0 >> 32);
-            ok[2] &= static_cast<uint32_t>(t1);
-            ok[3] &= static_cast<uint32_t>(t1 >> 32);
+            const uint32_t klo = static_cast<uint32_t>(K64), khi = static_cast<uint32_t>(K64 >> 32);
+            uint32_t a0, a1, b0, b1;
+            asm("sub.cc.u32 %0, %4, %6;\n\t"
+                "subc.u32 %1, %5, %7;\n\t"
+                "add.cc.u32 %0, %0, %8;\n\t"
+                "addc.u32 %1, %1, %9;\n\t"
+                "sub.cc.u32 %2, %10, %12;\n\t"
+                "subc.u32 %3, %11, %13;\n\t"
+                "add.cc.u32 %2, %2, %8;\n\t"
+                "addc.u32 %3, %3, %9;"
+                : "=&r"(a0), "=&r"(a1), "=&r"(b0), "=&r"(b1)
+                : "r"(cur.x), "r"(cur.y), "r"(prev.x), "r"(prev.y), "r"(klo), "r"(khi), "r"(cur.z), "r"(cur.w),
+                  "r"(prev.z), "r"(prev.w));
+            ok[0] &= a0;
+            ok[1] &= a1;
+            ok[2] &= b0;
+            ok[3] &= b1;
         } else if (PLANES == 2) {
             ok[0] &= cur.z - prev.x + 0x7fff7fffu;
             ok[1] &= cur.w - prev.y + 0x7fff7fffu;
