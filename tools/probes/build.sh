@@ -12,7 +12,7 @@ g++ -std=c++20 -O2 -I include -I $REF -I $JSON tools/probes/build_gen_compare.cp
   -o tools/probes/build_gen_compare_dropin
 g++ -std=c++20 -O2 -I $REF -I $JSON tools/probes/build_gen_compare.cpp -o tools/probes/build_gen_compare_ref
 g++ -std=c++17 -O2 tools/probes/startup_probe.cpp -ldl -o tools/probes/startup_probe
-for p in graph_update_probe launch_floor_probe gather_probe param_probe; do
+for p in graph_update_probe launch_floor_probe gather_probe param_probe launch_cost_probe; do
   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o tools/probes/$p tools/probes/$p.cu -lcuda
 done
 echo "probes built"
