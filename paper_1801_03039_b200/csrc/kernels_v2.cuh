@@ -890,13 +890,16 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
             if ((tile + 1) * RPG > p.n_rows || excl != 0u) vm = W::valid(r0, p.n_rows, excl, p.rank_k);
 
             if (p.debug_mode != 1) {
-                // Chunks longest first, statically: warp w takes the k-th
-                // longest for k = (w + 7 item) mod NCW + j NCW; the rotation
-                // evens each warp's share out over the tiles.  Each lane adds
-                // its own partial counts (16-bit halves: q = 0, 1) to a private
-                // word of the chunk -- no shuffles, no contended atomics.
+                // Chunks longest first, statically, in snake order: in round
+                // j warp w takes the k-th longest for k = j NCW + w' (j even)
+                // or j NCW + NCW - 1 - w' (j odd), w' = (w + 7 item) mod NCW;
+                // the rotation evens each warp's share out over the tiles.
+                // Each lane adds its own partial counts (16-bit halves: q = 0,
+                // 1) to a private word of the chunk -- no shuffles, no
+                // contended atomics.
                 const uint32_t n_here = c_hi - c_lo;
-                for (uint32_t k = (static_cast<uint32_t>(warp) + item * 7u) % NCW; k < n_here; k += NCW) {
+                const uint32_t wr = (static_cast<uint32_t>(warp) + item * 7u) % NCW;
+                for (uint32_t j = 0, k = wr; k < n_here; ++j, k = j * NCW + ((j & 1u) ? NCW - 1 - wr : wr)) {
                     const uint32_t ch = c_hi - 1 - k;
                     const uint32_t d = cdesc[ch];
                     uint32_t c;
