@@ -1049,9 +1049,13 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         // (rows x sum(len) x b bytes) -- no length sort, no cross-CTA sum
         const int sgrid = s.knobs.grid > 0 ? s.knobs.grid : 2 * s.sm_count;
         const double cell = c.layout == 4 ? 1.6 : c.layout == 3 ? 4.0 / 3.0 : c.layout == 2 ? 4.0 : 2.0;
+        // (auto: device-pointer calls only -- on the host path every CTA's
+        // results cross PCIe behind its own system fence, C1 e2e 32.5 us
+        // against K1v2's single final CTA)
         const bool use_s = !xacc && L <= size_t(kSMaxMine) * (size_t)sgrid &&
                            (s.knobs.split == 1 ||
-                            (s.knobs.split < 0 && !long_launch && double(s.rows) * L * cell <= kSplitMaxL2Bytes));
+                            (s.knobs.split < 0 && !done_flag && !long_launch &&
+                             double(s.rows) * L * cell <= kSplitMaxL2Bytes));
         s.last_grid = use_s ? sgrid : grid;
         s.last_cfg = c;
         s.last_collapsed = rl->collapsed;
