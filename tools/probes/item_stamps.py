@@ -1,6 +1,6 @@
 """Per-item timeline of CTA 0 in K1v2 (EBIC_PHASE_TIMING=1, device path):
 producer wait-for-free-stage / issue-done, consumer warp 0 wait-for-data /
-walk-done, for one workload.  usage: python tools/probes/item_stamps.py [c5ss]"""
+walk-done, for one workload.  usage: python tools/probes/item_stamps.py [c5ss] [host]"""
 import ctypes as C
 import os
 import sys
@@ -15,6 +15,7 @@ from paper_1801_03039_b200 import _lib  # noqa: E402
 from golden_io import trace  # noqa: E402
 
 t = trace(sys.argv[1] if len(sys.argv) > 1 else "c5ss")
+host = len(sys.argv) > 2 and sys.argv[2] == "host"  # the host-buffer API (CTA-0 population pull)
 off, cols, _, _ = t.batches[-1]
 with eb.Evaluator(t.matrix()) as ev:
     d_off = torch.from_numpy(off.astype(np.int64)).cuda()
@@ -23,8 +24,11 @@ with eb.Evaluator(t.matrix()) as ev:
     cnt = torch.zeros(P, dtype=torch.int64, device="cuda")
     fit = torch.zeros(P, dtype=torch.float64, device="cuda")
     for _ in range(4):
-        _lib.check(_lib.lib.ebic_count_matches_device(ev.handle, d_off.data_ptr(), d_cols.data_ptr(), P, L,
-                                                      t.eps, t.sigma, cnt.data_ptr(), fit.data_ptr(), None))
+        if host:
+            ev.evaluate_population(eb.CbfPopulation(off, cols), eb.FitnessParams(t.sigma), t.eps)
+        else:
+            _lib.check(_lib.lib.ebic_count_matches_device(ev.handle, d_off.data_ptr(), d_cols.data_ptr(), P, L,
+                                                          t.eps, t.sigma, cnt.data_ptr(), fit.data_ptr(), None))
         torch.cuda.synchronize()
     st = np.zeros((4096, 8), dtype=np.uint64)
     n = C.c_size_t(0)
