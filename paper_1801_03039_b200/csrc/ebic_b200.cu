@@ -129,8 +129,9 @@ struct Knobs {
         k.prefetch = env_int("EBIC_PREFETCH", 0);  // K1v2 compact: L2 prefetch distance (items)
         // K1v2: one-plane ranks packed three rows per word when they fit 9 bits
         k.pack = env_int("EBIC_PACK", 1);
-        // K1s (series-split kernel) for short single-shard launches: -1 auto, 0 off, 1 always
-        k.split = env_int("EBIC_SPLIT", -1);
+        // K1s (series-split kernel) for short single-shard launches: -1 auto, 0 off (default:
+        // with its tiles split over idle SMs K1v2 is faster at every BASELINE size), 1 always
+        k.split = env_int("EBIC_SPLIT", 0);
         return k;
     }
 };
@@ -1023,8 +1024,13 @@ void launch_count(ebic_ctx& ctx, Shard& s, const uint64_t* d_off, const uint16_t
         p.n_tiles = (uint32_t)((s.rows + c.rpg - 1) / c.rpg);
         const size_t smem = (size_t)s.max_smem - 1024;  // leaves room for the static shared bytes
         p.smem_window = (uint32_t)(smem - 128);
+        // fewer tiles than SMs: split every tile's chunks over up to
+        // max_parts CTAs (the kernel's last-wave split) instead of leaving
+        // SMs idle
         int grid = std::min<int>((int)p.n_tiles, s.sm_count);
-        if (s.knobs.grid > 0) grid = std::min<int>(s.knobs.grid, (int)p.n_tiles);
+        if ((int)p.n_tiles < s.sm_count)
+            grid = std::min<int>(s.sm_count, (int)p.n_tiles * std::max(1, s.knobs.max_parts));
+        if (s.knobs.grid > 0) grid = s.knobs.grid;
         p.gap = (uint32_t)std::min(std::max(s.knobs.gap, 0), 2);
         // 4-wide fp32 stripe reductions while every count is exact in fp32
         if (p.reduce_striped && s.rows < (1u << 24)) p.reduce_striped = 2;
