@@ -32,9 +32,10 @@ each rank counts its shard.  `e2e` (host buffers, the public C ABI) sums
 across ranks inside the count kernels: every rank's final CTA adds into rank
 0's accumulator through CUDA IPC peer memory and the last one writes counts +
 Eq. 1 into a shared-memory block all ranks read.  `value` (inputs resident in
-HBM, steps pipelined) all-reduces the counts with NCCL and runs the Eq. 1
-kernel on them (--reduce collective, default), or uses the in-kernel sum
-with a host wait per step (--reduce kernel).  Time = max over ranks.
+HBM) uses the same in-kernel sum with a host wait per step (--reduce kernel,
+default: one launch per step and no collective), or all-reduces the counts
+with NCCL and runs the Eq. 1 kernel on them (--reduce collective; also the
+fallback when CUDA IPC is unavailable).  Time = max over ranks.
 """
 from __future__ import annotations
 
@@ -813,10 +814,10 @@ def main():
     ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
                     help="torch.distributed backend (gloo: several ranks sharing one GPU, "
                          "kernel-side reduction only)")
-    ap.add_argument("--reduce", choices=["kernel", "collective"], default="collective",
+    ap.add_argument("--reduce", choices=["kernel", "collective"], default="kernel",
                     help="device-resident multi-process path (`value`): cross-rank sum in the count "
-                         "kernels, or NCCL (default: pipelines without host syncs); the e2e host "
-                         "path always sums inside the kernels")
+                         "kernels (default; one launch per step, host wait per step), or an NCCL "
+                         "all-reduce + Eq. 1 kernel; the e2e host path always sums inside the kernels")
     ap.add_argument("--force-sharded", action="store_true",
                     help="use the multi-process shard path (all-reduce + fitness kernel) even at N=1")
     ap.add_argument("--cpu-budget", type=float, default=15.0,
