@@ -978,6 +978,23 @@ struct RankWalker {
             ok[3] &= cur.w - prev.w + K;
         }
     }
+    // The packed 64-bit pair test with the constant known at compile time
+    // (STRICT: kStrict64, else kCollapsed64): cur + ~prev + (K + 1) equals
+    // cur - prev + K mod 2^64, which ptxas lowers to one three-input IADD3
+    // (two carry-outs, prev negated in the operand) + one IADD3.X per 64-bit
+    // word with K as immediates -- 2 integer instructions per word instead of
+    // the 3 of step()'s runtime-K carry chains.  Same bits as step().
+    template <bool STRICT>
+    __device__ __forceinline__ static void step_k(uint32_t* ok, const uint4& prev, const uint4& cur) {
+        static_assert(kPacked64, "64-bit packed layout only");
+        constexpr uint64_t K1 = (STRICT ? kStrict64 : kCollapsed64) + 1ull;
+        const uint64_t a = ((uint64_t(cur.y) << 32) | cur.x) + ~((uint64_t(prev.y) << 32) | prev.x) + K1;
+        const uint64_t b = ((uint64_t(cur.w) << 32) | cur.z) + ~((uint64_t(prev.w) << 32) | prev.z) + K1;
+        ok[0] &= static_cast<uint32_t>(a);
+        ok[1] &= static_cast<uint32_t>(a >> 32);
+        ok[2] &= static_cast<uint32_t>(b);
+        ok[3] &= static_cast<uint32_t>(b >> 32);
+    }
     __device__ __forceinline__ static uint32_t tally(const uint32_t* ok, const Mask& vm) {
         if constexpr (kPacked64) {  // result bits 11 + 12 f of each 64-bit word
             const uint64_t a = (uint64_t(ok[1]) << 32) | ok[0], b = (uint64_t(ok[3]) << 32) | ok[2];

@@ -9,7 +9,8 @@ usage: python tools/kernel_probe.py WORKLOAD [VARIANT ...]
 Per variant: a fresh context (knobs are read at creation), parity of counts
 and fitness against the reference trace (skipped for EBIC_DEBUG_MODE != 0),
 then per-launch CUDA-event times with L2 evicted before every launch (as
-bench.py's `value`) and back to back without eviction.  Prints one JSON line
+bench.py's `value`), the same without the eviction (warm L2), and back to
+back without eviction.  Prints one JSON line
 per variant."""
 import json
 import os
@@ -96,6 +97,16 @@ def main():
             evs[k][1].record(stream)
         torch.cuda.synchronize()
         per = [a.elapsed_time(b) * 1e3 for a, b in evs]
+        # same per-step events without the eviction: L2 keeps the code, the
+        # CBF, the rank tiles and the stripes (the GA's own case between
+        # generations); separates the cold-L2 cost from the launch floor
+        for k in range(n):
+            torch.cuda._sleep(100_000)
+            evs[k][0].record(stream)
+            step(bs[k % len(bs)])
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+        warm = [a.elapsed_time(b) * 1e3 for a, b in evs]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.sum(flush, dim=0, keepdim=True, out=sink)
         e0.record(stream)
@@ -107,6 +118,7 @@ def main():
         series = float(np.mean([b["P"] for b in bs]))
         print(json.dumps({"workload": name, "variant": var, "parity": parity,
                           "us_evicted_mean": float(np.mean(per)), "us_evicted_min": float(np.min(per)),
+                          "us_warm_mean": float(np.mean(warm)),
                           "us_back_to_back": e0.elapsed_time(e1) * 1e3 / n,
                           "mbic_per_s": series / float(np.mean(per)),
                           "rows_per_tile": info.rows_per_tile, "stages": info.stages,

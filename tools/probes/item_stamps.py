@@ -47,6 +47,9 @@ with eb.Evaluator(t.matrix()) as ev:
     q = lambda col: np.percentile((a[:, col] - t0) / 1e3, [0, 50, 100]).round(2).tolist()  # noqa: E731
     print("all CTAs (min/median/max us): start", q(0), "prologue end", q(1), "walk end", q(2),
           "reds done", q(4), "ticket", q(5), "end", q(3))
+    order = np.argsort(a[:, 2])[::-1][:6]  # the latest walks (CTA G-1 also fixes up the first dirty row)
+    print("latest walk ends (CTA: prologue end, walk end, us):",
+          [(int(c), round((a[c, 1] - t0) / 1e3, 2), round((a[c, 2] - t0) / 1e3, 2)) for c in order])
     last = a[a[:, 7] >= t0]  # (rows of CTAs that were last in earlier launches keep stale stamps)
     if len(last):
         k = int(np.argmax(last[:, 7]))
