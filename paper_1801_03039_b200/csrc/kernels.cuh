@@ -996,10 +996,15 @@ struct RankWalker {
         ok[3] &= static_cast<uint32_t>(b >> 32);
     }
     __device__ __forceinline__ static uint32_t tally(const uint32_t* ok, const Mask& vm) {
-        if constexpr (kPacked64) {  // result bits 11 + 12 f of each 64-bit word
-            const uint64_t a = (uint64_t(ok[1]) << 32) | ok[0], b = (uint64_t(ok[3]) << 32) | ok[2];
-            const uint64_t f = (a & kCollapsed64) | ((b & kCollapsed64) >> 1);
-            return __popc(static_cast<uint32_t>(f) & vm.m) + __popc(static_cast<uint32_t>(f >> 32) & vm.m_hi);
+        if constexpr (kPacked64) {
+            // result bits 11 + 12 f of each 64-bit word: 11, 23 in its low
+            // half, 3, 15, 27 in its high half -- disjoint, so both halves of
+            // both words fold into one 32-bit word (the second word's one bit
+            // down) and one POPC; the folded valid mask is m | m_hi.
+            constexpr uint32_t kLo = static_cast<uint32_t>(kCollapsed64), kHi = static_cast<uint32_t>(kCollapsed64 >> 32);
+            static_assert((kLo & kHi) == 0 && (((kLo | kHi) >> 1) & (kLo | kHi)) == 0, "disjoint result bits");
+            const uint32_t f = (ok[0] & kLo) | (ok[1] & kHi) | (((ok[2] & kLo) | (ok[3] & kHi)) >> 1);
+            return __popc(f & (vm.m | vm.m_hi));
         }
         constexpr uint32_t kRes = kPacked ? 0x20080200u : 0x80008000u;  // result bits of an ok word
         uint32_t f = ok[0] & kRes;
