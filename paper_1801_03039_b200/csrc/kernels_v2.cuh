@@ -888,6 +888,7 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
         // per item right before its walk
         const unsigned long long* excl_items = reinterpret_cast<const unsigned long long*>(smem + v.excl);
         uint32_t it = 0;  // this CTA's item number
+        uint32_t* const acc_lane = acc + lane;
         for (uint32_t item = blockIdx.x; item < n_items; item += G, ++it) {
             uint32_t tile = item, c_lo = 0, c_hi = n_chunks_s;
             if (item >= full) {  // a part of a last-wave tile: a chunk range
@@ -925,11 +926,11 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
                 // Each lane adds its own partial counts (16-bit halves: q = 0,
                 // 1) to a private word of the chunk -- no shuffles, no
                 // contended atomics.
-                const uint32_t n_here = c_hi - c_lo;
                 const uint32_t wr = (static_cast<uint32_t>(warp) + item * 7u) % NCW;
-                // (k steps alternate between dk and 2 NCW - dk)
-                for (uint32_t k = wr, dk = 2u * (NCW - 1u - wr) + 1u; k < n_here; k += dk, dk = 2u * NCW - dk) {
-                    const uint32_t ch = c_hi - 1 - k;
+                // k-th longest chunk = chunk c_hi - 1 - k, walked by its index
+                // directly (k steps alternate between dk and 2 NCW - dk)
+                for (int ch = static_cast<int>(c_hi - 1u - wr), dk = 2 * (NCW - 1 - static_cast<int>(wr)) + 1;
+                     ch >= static_cast<int>(c_lo); ch -= dk, dk = 2 * NCW - dk) {
                     const uint32_t d = cdesc[ch];
                     uint32_t c;
                     if (d) {
@@ -944,7 +945,7 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
                             if (g0 + q < P_slots)
                                 c |= W::count_any(base, wl.pcols + wl.sstart[g0 + q], wl.slen[g0 + q], vm) << (16 * q);
                     }
-                    atomicAdd(&acc[ch * 32 + lane], c);  // (no zero test: the branch costs more than the ATOMS)
+                    atomicAdd(acc_lane + ch * 32, c);  // (no zero test: the branch costs more than the ATOMS)
                 }
             }
             __syncwarp();

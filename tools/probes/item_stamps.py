@@ -1,6 +1,6 @@
 """Per-item timeline of CTA 0 in K1v2 (EBIC_PHASE_TIMING=1, device path):
 producer wait-for-free-stage / issue-done, consumer warp 0 wait-for-data /
-walk-done, for one workload.  usage: python tools/probes/item_stamps.py [c5ss] [host]"""
+walk-done, for one workload.  usage: python tools/probes/item_stamps.py [c5ss] [host] [rows=N]"""
 import ctypes as C
 import os
 import sys
@@ -15,9 +15,10 @@ from paper_1801_03039_b200 import _lib  # noqa: E402
 from golden_io import trace  # noqa: E402
 
 t = trace(sys.argv[1] if len(sys.argv) > 1 else "c5ss")
-host = len(sys.argv) > 2 and sys.argv[2] == "host"  # the host-buffer API (CTA-0 population pull)
+host = "host" in sys.argv[2:]  # the host-buffer API (CTA-0 population pull)
+rows = [int(a[5:]) for a in sys.argv[2:] if a.startswith("rows=")]  # rows=N: the first N rows only (a shard's size)
 off, cols, _, _ = t.batches[-1]
-with eb.Evaluator(t.matrix()) as ev:
+with eb.Evaluator(t.matrix()[:rows[0]] if rows else t.matrix()) as ev:
     d_off = torch.from_numpy(off.astype(np.int64)).cuda()
     d_cols = torch.from_numpy(cols.view(np.int16)).cuda()
     P, L = len(off) - 1, int(off[-1])
