@@ -980,10 +980,11 @@ struct RankWalker {
     }
     // The packed 64-bit pair test with the constant known at compile time
     // (STRICT: kStrict64, else kCollapsed64): cur + ~prev + (K + 1) equals
-    // cur - prev + K mod 2^64, which ptxas lowers to one three-input IADD3
-    // (two carry-outs, prev negated in the operand) + one IADD3.X per 64-bit
-    // word with K as immediates -- 2 integer instructions per word instead of
-    // the 3 of step()'s runtime-K carry chains.  Same bits as step().
+    // cur - prev + K mod 2^64, which ptxas lowers, with K as immediates, to
+    // a three-input IADD3 (two carry-outs, prev negated in the operand) for
+    // the low half and IADD3.X + IMAD.IADD for the high half -- 2
+    // integer-pipe instructions per 64-bit word (the IMAD issues on the FMA
+    // pipe) instead of step()'s 3.  Same bits as step().
     template <bool STRICT>
     __device__ __forceinline__ static void step_k(uint32_t* ok, const uint4& prev, const uint4& cur) {
         static_assert(kPacked64, "64-bit packed layout only");
