@@ -351,7 +351,6 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
             run += t;
         }
     }
-    if (cols_ready) mbar_wait(cols_ready, 0);  // producer: bitmap + slot bases (compact staging)
     named_bar_sync(bar_id, nthreads);  // 3
     if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 600 + 3] = global_ns();
 
@@ -428,6 +427,9 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
     // dummies).  A series-per-thread fill would leave the longest series (and
     // its slot look-ups) on the critical path.
     if (compact) {
+        // the producers' column set (bitmap + slot bases) is needed from
+        // here on only: placement above ran while they built it
+        mbar_wait(cols_ready, 0);
         named_bar_sync(bar_id, nthreads);  // 4a
         if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 601 + 2] = global_ns();
         const uint32_t n_quads = w.hpad[kLenBuckets - 1] / 4;
