@@ -312,11 +312,11 @@ void grow_pinned(unsigned char** p, size_t* cap, size_t need) {
 
 // Reduction scratch of one count launch: striped accumulators [P][kStripes]
 // (zero between launches) or the tree's (grid + groups) rows of P counters.
-// mode: 0 tree, 1 u32 stripes [P][8], 2 fp32 stripes [8][P rounded to 4] (K1v2)
+// mode: 0 tree, 1 u32 stripes [P][8], 2 fp32 stripes [kV2Stripes][slots rounded to 8] (K1v2)
 void ensure_partial(Shard& s, size_t P, int grid, int mode) {
     const size_t gsz = reduce_group_size((uint32_t)grid);
     const size_t need = mode == 3 ? 2 * P  // K1s: split-series counts + arrival counters
-                        : mode == 2 ? ((P + kV2Pad + 7) & ~size_t(7)) * kStripes  // slots incl. dummies, whole chunks
+                        : mode == 2 ? ((P + kV2Pad + 7) & ~size_t(7)) * kV2Stripes  // slots incl. dummies, whole chunks
                         : mode == 1 ? P * kStripes : (size_t(grid) + (grid + gsz - 1) / gsz) * P;
     if (need <= s.partial_cap && mode == s.last_reduce) return;
     // a launch still queued on the previous stream may use the old scratch

@@ -45,6 +45,12 @@ constexpr int kV2MaxStages = 4;
 constexpr uint32_t kV2MaxUnroll = EBIC_V2_MAX_UNROLL;
 static_assert(kV2MaxUnroll >= 3 && kV2MaxUnroll <= 12, "unrolled chunk lengths 2..3+");
 constexpr uint32_t kV2ExclItems = 64;  // per-CTA items whose excl words are preloaded
+// Stripes of the slot-order tail's fp32 accumulators.  One: 148 CTAs' 4-wide
+// reductions per slot quad contend less than the final CTA's extra loads cost
+// (same box, L2 evicted / warm / back to back, us: C4 20.71 / 18.46 / 15.62
+// with 8 stripes, 20.59 / 18.35 / 15.18 with 4, 20.47 / 17.93 / 14.98 with 1;
+// C5 68.1 -> 67.4 evicted; profiles/r02_walk_ab.log, ab12-ab14).
+constexpr int kV2Stripes = 1;
 
 // Byte offsets of the persistent work list inside the dynamic window.
 struct V2Layout {
@@ -555,7 +561,7 @@ __device__ __forceinline__ uint32_t v2_count_chunk(uint32_t L, uint32_t base, co
     }
 }
 
-// Cross-CTA tail in slot order (see the kernel).  Stripes [kStripes][PS4]
+// Cross-CTA tail in slot order (see the kernel).  Stripes [kV2Stripes][PS4]
 // fp32, PS4 = the slot count rounded to a whole chunk (the host sizes them for P + kV2Pad
 // slots); integer counts below 2^24 are exact in fp32.
 template <int GL, int SPG, uint32_t CHUNK>
@@ -564,7 +570,7 @@ __device__ __forceinline__ void v2_tail_slots(const CountParams& p, const WorkLi
     static_assert(GL == 8 && SPG == 2 && CHUNK == 8, "chunk = 4 groups x 2 slots");
     const uint32_t PS4 = (p.n_series + kV2Pad + 7u) & ~7u;  // whole chunks
     float* stripes = reinterpret_cast<float*>(p.partial);
-    const uint32_t stripe = blockIdx.x % kStripes;
+    const uint32_t stripe = blockIdx.x % kV2Stripes;
     unsigned long long* stamp = p.phase_ns ? p.phase_ns + 8ull * blockIdx.x : nullptr;
     // One thread per 4 consecutive slots: chunk q / 2, lane groups 2 (q % 2)
     // and 2 (q % 2) + 1 -- sixteen consecutive per-lane words (low / high
@@ -601,14 +607,14 @@ __device__ __forceinline__ void v2_tail_slots(const CountParams& p, const WorkLi
     if (!s_last) return;
     if (stamp && threadIdx.x == 0) stamp[7] = global_ns();
     for (uint32_t g = threadIdx.x; g < P_slots; g += blockDim.x) {
-        float v[kStripes];
+        float v[kV2Stripes];
 #pragma unroll
-        for (int k = 0; k < kStripes; ++k) v[k] = __ldcg(stripes + size_t(k) * PS4 + g);
+        for (int k = 0; k < kV2Stripes; ++k) v[k] = __ldcg(stripes + size_t(k) * PS4 + g);
         double t = 0.0;
 #pragma unroll
-        for (int k = 0; k < kStripes; ++k) t += static_cast<double>(v[k]);
+        for (int k = 0; k < kV2Stripes; ++k) t += static_cast<double>(v[k]);
 #pragma unroll
-        for (int k = 0; k < kStripes; ++k) __stcg(stripes + size_t(k) * PS4 + g, 0.0f);
+        for (int k = 0; k < kV2Stripes; ++k) __stcg(stripes + size_t(k) * PS4 + g, 0.0f);
         const uint32_t s = wl.sl[g];
         if (s == 0xffffffffu) continue;  // dummy slot
         const uint64_t c = static_cast<uint64_t>(t);
@@ -733,7 +739,7 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
         if (pw == 0 && lane == 2 && p.reduce_striped == 2) {
             // this CTA's share of the slot stripes, so the tail's reductions
             // (and the release before its ticket) do not wait on DRAM fills
-            const uint64_t bytes = uint64_t(kStripes) * ((P + kV2Pad + 7u) & ~7u) * 4u;
+            const uint64_t bytes = uint64_t(kV2Stripes) * ((P + kV2Pad + 7u) & ~7u) * 4u;
             const uint64_t per = ((bytes + gridDim.x - 1) / gridDim.x + 127) & ~uint64_t(127);
             const uint64_t lo = per * blockIdx.x;
             if (lo < bytes) {
@@ -959,7 +965,7 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
     if (stamp && threadIdx.x == 0) stamp[2] = global_ns();
     if (p.reduce_striped == 2) {
         // Slot-order tail: every CTA builds the same slot order, so the
-        // stripes are indexed by slot ([8][whole chunks] fp32) and a
+        // stripes are indexed by slot ([kV2Stripes][whole chunks] fp32) and a
         // chunk's 8 slot counts go out as two 4-wide reductions straight
         // from the lane sums -- no series-order scatter; the last CTA maps
         // slots to series.
