@@ -44,6 +44,18 @@ constexpr int kV2MaxStages = 4;
 // (profiles/r02_kernel_variants.log); C4 unchanged.
 constexpr uint32_t kV2MaxUnroll = EBIC_V2_MAX_UNROLL;
 static_assert(kV2MaxUnroll >= 3 && kV2MaxUnroll <= 12, "unrolled chunk lengths 2..3+");
+// The 10-bit packed layout (C <= 510: C1-C4) unrolls lengths 2..6 only: its
+// launches walk one or two tiles per SM with a cold instruction cache (L2
+// evicted between steps), so less walk code beats unrolled lengths 7-8 there
+// (C4 19.9 -> 18.7 us per step, L2 evicted), while C5's long launches keep
+// 2..8 (6: 61.8 -> 62.6 us back to back; profiles/r02_walk_ab.log, ab15).
+#ifndef EBIC_V2_MAX_UNROLL_P10
+#define EBIC_V2_MAX_UNROLL_P10 6
+#endif
+template <class W>
+__host__ __device__ constexpr uint32_t v2_max_unroll() {
+    return W::kPacked ? (EBIC_V2_MAX_UNROLL_P10 < kV2MaxUnroll ? EBIC_V2_MAX_UNROLL_P10 : kV2MaxUnroll) : kV2MaxUnroll;
+}
 constexpr uint32_t kV2ExclItems = 64;  // per-CTA items whose excl words are preloaded
 // Stripes of the slot-order tail's fp32 accumulators.  One: 148 CTAs' 4-wide
 // reductions per slot quad contend less than the final CTA's extra loads cost
@@ -260,7 +272,7 @@ __device__ __forceinline__ void v2_build_columns(const CountParams& p, unsigned 
 // Consumer-side work list (NCW warps): the v1 counting sort by length
 // (build_work_list phases A-C), then lists of slot byte offsets (slot x 128)
 // once the producer's column slots are ready, then chunk descriptors.
-template <int CHUNK>
+template <int CHUNK, uint32_t MAXU>
 __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigned char* smem, const V2Layout& v,
                                                    const WorkList& w, uint64_t* cols_ready, int tid, int nthreads,
                                                    int bar_id, uint32_t n_items, uint32_t full, uint32_t parts,
@@ -341,7 +353,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
         for (int k = 0; k < 2; ++k) {
             const int b = tid + 32 * k;
             uint32_t c = orig[b];
-            if (b >= 2 && b <= kV2MaxUnroll) c = (c + CHUNK - 1) / CHUNK * CHUNK;
+            if (b >= 2 && b <= MAXU) c = (c + CHUNK - 1) / CHUNK * CHUNK;
             if (b == 1) c = (orig[0] + orig[1] + CHUNK - 1) / CHUNK * CHUNK - orig[0];
             w.hist[b] = c;
             w.hpad[b] = b < kLenBuckets - 1 ? c * pad4(b) : 0u;
@@ -384,7 +396,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
                 // stride pad4(length)) and the length is unrolled (2..kV2MaxUnroll); else
                 // 0 (per-slot path).  Bucket b ends where bucket b + 1 starts.
                 const uint32_t end = w.hist[bkt + 1];
-                const bool uni = g + CHUNK <= end && len >= 2 && len <= kV2MaxUnroll;
+                const bool uni = g + CHUNK <= end && len >= 2 && len <= MAXU;
                 reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = uni ? ((st << 8) | len) : 0u;
             }
             if (compact) {
@@ -424,7 +436,7 @@ __device__ __forceinline__ void v2_build_work_list(const CountParams& p, unsigne
             else reinterpret_cast<uint4*>(w.pcols)[st / 4 + q] = make_uint4(0u, 0u, 0u, 0u);
         }
         if (g % CHUNK == 0)
-            reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = (b >= 2 && b <= kV2MaxUnroll) ? ((st << 8) | b) : 0u;
+            reinterpret_cast<uint32_t*>(smem + v.cdesc)[g / CHUNK] = (b >= 2 && b <= MAXU) ? ((st << 8) | b) : 0u;
     }
     if (tid == 0) reinterpret_cast<uint32_t*>(smem + v.misc)[3] = pslots;
     if (p.phase_ns && blockIdx.x == 0 && tid == 0) p.phase_ns[8 * 601 + 1] = global_ns();
@@ -528,7 +540,7 @@ __device__ __forceinline__ uint32_t v2_count_uniform(uint32_t L, uint32_t base, 
                                                      const typename W::Mask& vm) {
     // (lengths above kV2MaxUnroll never get a uniform descriptor; their cases
     // alias the longest instantiation so no extra walk code is generated)
-    constexpr uint32_t M = kV2MaxUnroll;
+    constexpr uint32_t M = v2_max_unroll<W>();
     switch (L) {
         case 2: return v2_count2<W, 2, KS>(base, pc, stride, vm);
         case 3: return v2_count2<W, 3, KS>(base, pc, stride, vm);
@@ -857,7 +869,7 @@ __global__ void __launch_bounds__((NCW + NP) * 32, 1)
             }
         }
         if (p.phase_ns && blockIdx.x == 0 && threadIdx.x == 0) p.phase_ns[8 * 600] = global_ns();
-        v2_build_work_list<CHUNK>(p, smem, v, wl, compact ? cols_ready : nullptr, threadIdx.x, NCW * 32, 1,
+        v2_build_work_list<CHUNK, v2_max_unroll<W>()>(p, smem, v, wl, compact ? cols_ready : nullptr, threadIdx.x, NCW * 32, 1,
                                   n_items, full, parts, RPG);
         if (threadIdx.x == 0) mbar_arrive(prol_bar);
         if (stamp && threadIdx.x == 0) stamp[1] = global_ns();
